@@ -1,0 +1,718 @@
+// C ABI of trackforge_b200 (declared in include/trackforge_b200.h).
+//
+// Owns the device-resident per-stream track tables, the per-frame detection
+// buffers and the launch sequence of one update:
+//   [host input only] cudaMemcpy2DAsync of the 8 confidence planes per scale
+//   frame_heads_kernel  (S*B CTAs)   decode + NMS + gather/normalise
+//   associate_kernel    (S CTAs)     B frames per stream, sequential per stream
+//   [host output only] cudaMemcpyAsync of the records
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "tf_kernels.cuh"
+
+using namespace tfd;
+
+struct tf_ctx {
+  tf_config cfg;
+  tf_capacity cap;
+  int device;
+  Params P;
+  std::string err;
+  int cap_entries;
+  // per-frame detection buffers
+  DetBuf det;
+  long long* d_frame_index;
+  // per-stream track tables
+  TrackBuf trk;
+  int16_t* pool_col;
+  int16_t* pool_row;
+  double* pool_val;
+  // host mirror of each stream's last stepped frame (ordering checks)
+  std::vector<long long> last_frame;
+  std::vector<long long> frame_scratch;
+  // device staging used when inputs / outputs are host memory
+  float* stage_conf[3];
+  size_t stage_conf_elems[3];
+  int* rec_count;
+  long long* rec_id;
+  double* rec_box;
+  double* rec_obj;
+  int rec_capacity;
+  // streams touched by the last update (for tf_finish)
+  int last_begin, last_count;
+  // optional per-kernel CUDA-event timing (bench.py roofline)
+  int profiling;
+  std::vector<cudaEvent_t> events;   // triples: before frame kernel, after it, after associate
+  size_t events_used;
+  long long prof_bytes_frame, prof_frames;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+const char* kNames[] = {"OK",
+                        "InvalidBoxError",
+                        "InvalidMeasurementError",
+                        "DimensionError",
+                        "DegenerateEmbeddingError",
+                        "PrecisionOverflowError",
+                        "LayoutError",
+                        "ConfigError",
+                        "OrderingError",
+                        "NumericError",
+                        "CapacityError",
+                        "CudaError",
+                        "ArgumentError"};
+
+int fail(tf_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define TF_CUDA(ctx, expr)                                                                 \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) return fail((ctx), TF_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+cudaError_t dev_alloc(tf_ctx* c, T** p, size_t n) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, n * sizeof(T) > 0 ? n * sizeof(T) : 16);
+  if (e == cudaSuccess) {
+    c->allocs.push_back(q);
+    *p = static_cast<T*>(q);
+  }
+  return e;
+}
+
+Params make_params(const tf_config& c) {
+  Params p;
+  p.conf_threshold = c.conf_threshold;
+  if (c.conf_threshold <= 0.0)
+    p.conf_logit = -INFINITY;
+  else if (c.conf_threshold >= 1.0)
+    p.conf_logit = INFINITY;
+  else
+    p.conf_logit = std::log(c.conf_threshold) - std::log1p(-c.conf_threshold);
+  p.nms_iou = c.nms_iou;
+  p.max_cost = c.max_cost;
+  p.gate_threshold = c.gate_threshold;
+  p.alpha = c.smoothing_alpha;
+  p.beta = 1.0 - c.smoothing_alpha;
+  p.wp = c.std_weight_position;
+  p.wv = c.std_weight_velocity;
+  p.std_aspect = c.std_aspect;
+  p.std_aspect_velocity = c.std_aspect_velocity;
+  p.std_aspect_measurement = c.std_aspect_measurement;
+  p.gate_metric = c.gate_metric;
+  p.max_lost = c.max_lost;
+  p.min_hits = c.min_hits;
+  p.dim = c.embedding_dim;
+  p.quantize = c.quantize_binary16;
+  return p;
+}
+
+// Configuration checks the reference performs on every step (filter_confidence
+// tf/postproc.py:63-64, nms tf/postproc.py:76-77).
+int check_step_config(tf_ctx* c) {
+  const tf_config& g = c->cfg;
+  if (!(g.conf_threshold >= 0.0 && g.conf_threshold <= 1.0))
+    return fail(c, TF_CONFIG, "confidence threshold must be in [0, 1], got " + std::to_string(g.conf_threshold));
+  if (!(g.nms_iou > 0.0 && g.nms_iou < 1.0))
+    return fail(c, TF_CONFIG, "NMS IoU threshold must be in (0, 1), got " + std::to_string(g.nms_iou));
+  return TF_OK;
+}
+
+__global__ void reset_streams_kernel(TrackBuf t, int s0, int n, int cap_tracks) {
+  const int s = s0 + blockIdx.x;
+  if (blockIdx.x >= n) return;
+  for (int i = threadIdx.x; i < cap_tracks; i += blockDim.x)
+    t.free_stack[static_cast<long long>(s) * cap_tracks + i] = cap_tracks - 1 - i;
+  if (threadIdx.x == 0) {
+    t.n_free[s] = cap_tracks;
+    t.n_tracks[s] = 0;
+    t.next_id[s] = 1;
+    t.last_frame[s] = LLONG_MIN;
+    t.status[s] = 0;
+  }
+}
+
+int check_ordering(tf_ctx* c, int s, const long long* frames, int B) {
+  long long prev = c->last_frame[s];
+  for (int b = 0; b < B; ++b) {
+    if (prev != std::numeric_limits<long long>::min() && frames[b] <= prev)
+      return fail(c, TF_ORDERING, "stream " + std::to_string(s) + ": frame " + std::to_string(frames[b]) +
+                                      " does not advance past " + std::to_string(prev));
+    prev = frames[b];
+  }
+  return TF_OK;
+}
+
+TraceBuf to_trace(const tf_trace* t) {
+  TraceBuf b{};
+  if (t) {
+    b.cand_count = t->cand_count;
+    b.det_count = t->det_count;
+    b.det_code = t->det_code;
+    b.det_track = reinterpret_cast<long long*>(t->det_track);
+    b.det_cost = t->det_cost;
+    b.det_matched = t->det_matched;
+  }
+  // associate_kernel writes the per-detection trace only when all three exist
+  if (!(b.det_track && b.det_cost && b.det_matched)) {
+    b.det_track = nullptr;
+    b.det_cost = nullptr;
+    b.det_matched = nullptr;
+  }
+  return b;
+}
+
+__global__ void copy_codes_kernel(const int* count, const int* code, int* out, int frames, int cap_det) {
+  const int f = blockIdx.x;
+  if (f >= frames) return;
+  const int n = count[f];
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    out[static_cast<long long>(f) * cap_det + k] = code[static_cast<long long>(f) * cap_det + k];
+}
+
+cudaError_t prof_mark(tf_ctx* c, int which, cudaStream_t st) {
+  if (!c->profiling) return cudaSuccess;
+  const size_t idx = c->events_used + which;
+  while (c->events.size() <= idx) {
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreate(&e);
+    if (r != cudaSuccess) return r;
+    c->events.push_back(e);
+  }
+  cudaError_t r = cudaEventRecord(c->events[idx], st);
+  if (which == 2) c->events_used += 3;
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tf_version(void) { return 1; }
+
+const char* tf_status_name(int status) {
+  if (status < 0 || status > TF_ARGUMENT) return "UnknownError";
+  return kNames[status];
+}
+
+const char* tf_last_error(const tf_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t device, tf_ctx** out) {
+  if (!config || !capacity || !out) return TF_ARGUMENT;
+  *out = nullptr;
+  const tf_capacity& k = *capacity;
+  if (k.streams < 1 || k.max_frames < 1 || k.max_candidates < 1 || k.max_candidates > 1024 ||
+      k.max_detections < 1 || k.max_detections > 1024 || k.max_tracks < 1 || k.max_tracks > 1024 ||
+      config->embedding_dim < 1)
+    return TF_ARGUMENT;
+  tf_ctx* c = new tf_ctx();
+  c->cfg = *config;
+  c->cap = k;
+  c->device = device;
+  c->P = make_params(*config);
+  c->last_begin = 0;
+  c->last_count = 0;
+  c->rec_capacity = 0;
+  c->rec_count = nullptr;
+  c->profiling = 0;
+  c->events_used = 0;
+  c->prof_bytes_frame = 0;
+  c->prof_frames = 0;
+  for (int i = 0; i < 3; ++i) {
+    c->stage_conf[i] = nullptr;
+    c->stage_conf_elems[i] = 0;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete c;
+    return TF_CUDA;
+  }
+  const size_t S = k.streams, F = k.max_frames, Km = k.max_detections, Tm = k.max_tracks,
+               D = config->embedding_dim;
+  // shared-memory budget for the association CTA decides how many CSR entries stay on chip
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  int entries = 2048;
+  while (entries > 64 && assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + 2048 > static_cast<size_t>(smem_optin))
+    entries /= 2;
+  if (assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + 2048 > static_cast<size_t>(smem_optin) ||
+      frame_smem_bytes(54264, k.max_candidates) + 2048 > static_cast<size_t>(smem_optin)) {
+    delete c;
+    return TF_ARGUMENT;
+  }
+  c->cap_entries = entries;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](auto** p, size_t n) {
+    if (e == cudaSuccess) e = dev_alloc(c, p, n);
+  };
+  A(&c->det.count, F);
+  A(&c->det.cand_count, F);
+  A(&c->det.status, F);
+  A(&c->det.meas, F * Km * 4);
+  A(&c->det.obj, F * Km);
+  A(&c->det.code, F * Km);
+  A(&c->det.emb, F * Km * D);
+  A(&c->d_frame_index, F);
+  A(&c->trk.id, S * Tm);
+  A(&c->trk.state, S * Tm);
+  A(&c->trk.hits, S * Tm);
+  A(&c->trk.lost, S * Tm);
+  A(&c->trk.last, S * Tm);
+  A(&c->trk.slot, S * Tm);
+  A(&c->trk.mean, S * Tm * 8);
+  A(&c->trk.cov, S * Tm * 12);
+  A(&c->trk.emb_pool, S * Tm * D);
+  A(&c->trk.free_stack, S * Tm);
+  A(&c->trk.n_free, S);
+  A(&c->trk.n_tracks, S);
+  A(&c->trk.next_id, S);
+  A(&c->trk.last_frame, S);
+  A(&c->trk.status, S);
+  A(&c->pool_col, S * Tm * Km);
+  A(&c->pool_row, S * Tm * Km);
+  A(&c->pool_val, S * Tm * Km);
+  if (e != cudaSuccess) {
+    std::string m = cudaGetErrorString(e);
+    tf_destroy(c);
+    return TF_CUDA;
+  }
+  c->last_frame.assign(S, std::numeric_limits<long long>::min());
+  reset_streams_kernel<<<static_cast<unsigned>(S), 256>>>(c->trk, 0, static_cast<int>(S), k.max_tracks);
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    tf_destroy(c);
+    return TF_CUDA;
+  }
+  *out = c;
+  return TF_OK;
+}
+
+int tf_destroy(tf_ctx* ctx) {
+  if (!ctx) return TF_OK;
+  cudaSetDevice(ctx->device);
+  for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+  for (void* p : ctx->allocs) cudaFree(p);
+  delete ctx;
+  return TF_OK;
+}
+
+int tf_reset_stream(tf_ctx* c, int32_t stream, void* cuda_stream) {
+  if (!c) return TF_ARGUMENT;
+  if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  reset_streams_kernel<<<1, 256, 0, st>>>(c->trk, stream, 1, c->cap.max_tracks);
+  TF_CUDA(c, cudaGetLastError());
+  c->last_frame[stream] = std::numeric_limits<long long>::min();
+  return TF_OK;
+}
+
+static int ensure_record_staging(tf_ctx* c, int frames, int max_records) {
+  const int need = frames * max_records;
+  if (need <= c->rec_capacity && c->rec_count) return TF_OK;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](auto** p, size_t n) {
+    if (e == cudaSuccess) e = dev_alloc(c, p, n);
+  };
+  A(&c->rec_count, static_cast<size_t>(c->cap.max_frames));
+  A(&c->rec_id, static_cast<size_t>(need));
+  A(&c->rec_box, static_cast<size_t>(need) * 4);
+  A(&c->rec_obj, static_cast<size_t>(need));
+  if (e != cudaSuccess) return fail(c, TF_CUDA, std::string("record staging: ") + cudaGetErrorString(e));
+  c->rec_capacity = need;
+  return TF_OK;
+}
+
+int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int32_t n_streams,
+                    int32_t B, const int64_t* frame_index, const tf_records* out, const tf_trace* trace,
+                    void* cuda_stream) {
+  if (!c || !heads || !frame_index || !out) return fail(c, TF_ARGUMENT, "null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  if (n_streams < 1 || B < 1 || stream_begin < 0 || stream_begin + n_streams > c->cap.streams)
+    return fail(c, TF_ARGUMENT, "stream range out of bounds");
+  const int F = n_streams * B;
+  if (F > c->cap.max_frames) return fail(c, TF_CAPACITY, "frames per update exceed max_frames");
+  if (out->max_records < 1) return fail(c, TF_ARGUMENT, "max_records must be >= 1");
+  int rc = check_step_config(c);
+  if (rc) return rc;
+  for (int i = 0; i < 3; ++i) {
+    const tf_head_scale& s = heads->scale[i];
+    if (!s.head || !s.emb || s.height < 1 || s.width < 1 || s.head_stride_c < static_cast<long long>(s.height) * s.width)
+      return fail(c, TF_LAYOUT, "head scale " + std::to_string(i) + ": bad pointer or layout");
+  }
+  for (int ls = 0; ls < n_streams; ++ls) {
+    rc = check_ordering(c, stream_begin + ls, reinterpret_cast<const long long*>(frame_index) + static_cast<size_t>(ls) * B, B);
+    if (rc) return rc;
+  }
+  TF_CUDA(c, cudaSetDevice(c->device));
+  TF_CUDA(c, cudaMemcpyAsync(c->d_frame_index, frame_index, sizeof(long long) * F, cudaMemcpyHostToDevice, st));
+
+  HeadLaunch h;
+  h.heads = heads;
+  h.frames = F;
+  h.cap_cand = c->cap.max_candidates;
+  h.cap_det = c->cap.max_detections;
+  h.det = c->det;
+  tf_heads staged = *heads;
+  if (heads->host_memory) {
+    // Confidence planes (channels 4,5 of every anchor) go over PCIe with the copy
+    // engine; box deltas of candidates and the embeddings of every candidate are
+    // read in place through the mapped host pointer by the frame kernel.
+    for (int i = 0; i < 3; ++i) {
+      const tf_head_scale& s = heads->scale[i];
+      const size_t hw = static_cast<size_t>(s.height) * s.width;
+      const size_t need = static_cast<size_t>(F) * 24 * hw;
+      if (c->stage_conf_elems[i] < need) {
+        float* p = nullptr;
+        TF_CUDA(c, dev_alloc(c, &p, need));
+        c->stage_conf[i] = p;
+        c->stage_conf_elems[i] = need;
+      }
+      // staging keeps the [F][24][H][W] geometry; only conf planes are filled.
+      // Rows of the 2D copy are (frame, anchor) pairs of 2 planes each; frames
+      // with a uniform stride collapse into one copy per scale.
+      const bool uniform = s.head_stride_n == 4 * (6 * s.head_stride_c);
+      const int calls = uniform ? 1 : F;
+      const int rows = uniform ? 4 * F : 4;
+      for (int f = 0; f < calls; ++f) {
+        const float* src = s.head + static_cast<long long>(f) * s.head_stride_n + 4 * s.head_stride_c;
+        float* dst = c->stage_conf[i] + static_cast<size_t>(f) * 24 * hw + 4 * hw;
+        TF_CUDA(c, cudaMemcpy2DAsync(dst, 6 * hw * sizeof(float), src, 6 * s.head_stride_c * sizeof(float),
+                                     2 * hw * sizeof(float), rows, cudaMemcpyHostToDevice, st));
+      }
+      staged.scale[i].head_stride_n = static_cast<long long>(24 * hw);
+      staged.scale[i].head_stride_c = static_cast<long long>(hw);
+      h.head_ptr[i] = c->stage_conf[i];
+      void* dptr = nullptr;
+      TF_CUDA(c, cudaHostGetDevicePointer(&dptr, const_cast<float*>(s.emb), 0));
+      h.emb_ptr[i] = static_cast<const float*>(dptr);
+    }
+    h.heads = &staged;
+    rc = TF_OK;
+  } else {
+    for (int i = 0; i < 3; ++i) {
+      h.head_ptr[i] = heads->scale[i].head;
+      h.emb_ptr[i] = heads->scale[i].emb;
+    }
+  }
+  // In host mode the deltas are read from the mapped host tensor: pass its
+  // device alias and original strides through a second descriptor.
+  if (heads->host_memory) {
+    for (int i = 0; i < 3; ++i) {
+      void* dptr = nullptr;
+      TF_CUDA(c, cudaHostGetDevicePointer(&dptr, const_cast<float*>(heads->scale[i].head), 0));
+      h.delta_ptr[i] = static_cast<const float*>(dptr);
+      h.delta_stride_n[i] = heads->scale[i].head_stride_n;
+      h.delta_stride_c[i] = heads->scale[i].head_stride_c;
+    }
+  } else {
+    for (int i = 0; i < 3; ++i) {
+      h.delta_ptr[i] = heads->scale[i].head;
+      h.delta_stride_n[i] = heads->scale[i].head_stride_n;
+      h.delta_stride_c[i] = heads->scale[i].head_stride_c;
+    }
+  }
+  TF_CUDA(c, prof_mark(c, 0, st));
+  TF_CUDA(c, launch_frame_heads(h, c->P, st));
+  TF_CUDA(c, prof_mark(c, 1, st));
+
+  AssocArgs a;
+  a.det = c->det;
+  a.trk = c->trk;
+  a.trace = to_trace(trace);
+  a.frame_index = c->d_frame_index;
+  a.stream_begin = stream_begin;
+  a.B = B;
+  a.cap_tracks = c->cap.max_tracks;
+  a.cap_det = c->cap.max_detections;
+  a.cap_entries = c->cap_entries;
+  a.pool_col = c->pool_col;
+  a.pool_row = c->pool_row;
+  a.pool_val = c->pool_val;
+  const bool host_out = heads->host_memory != 0;
+  if (host_out) {
+    rc = ensure_record_staging(c, F, out->max_records);
+    if (rc) return rc;
+    a.out.count = c->rec_count;
+    a.out.track_id = c->rec_id;
+    a.out.box = c->rec_box;
+    a.out.objectness = c->rec_obj;
+  } else {
+    a.out.count = out->count;
+    a.out.track_id = reinterpret_cast<long long*>(out->track_id);
+    a.out.box = out->box;
+    a.out.objectness = out->objectness;
+  }
+  a.out.max_records = out->max_records;
+  TF_CUDA(c, launch_associate(a, n_streams, c->P, st));
+  TF_CUDA(c, prof_mark(c, 2, st));
+  if (trace && trace->det_code)
+    copy_codes_kernel<<<F, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, F, c->cap.max_detections);
+  if (host_out) {
+    const size_t n = static_cast<size_t>(F) * out->max_records;
+    TF_CUDA(c, cudaMemcpyAsync(out->count, c->rec_count, sizeof(int) * F, cudaMemcpyDeviceToHost, st));
+    TF_CUDA(c, cudaMemcpyAsync(out->track_id, c->rec_id, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
+    TF_CUDA(c, cudaMemcpyAsync(out->box, c->rec_box, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, st));
+    TF_CUDA(c, cudaMemcpyAsync(out->objectness, c->rec_obj, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  }
+  for (int ls = 0; ls < n_streams; ++ls)
+    c->last_frame[stream_begin + ls] = frame_index[static_cast<size_t>(ls) * B + B - 1];
+  c->last_begin = stream_begin;
+  c->last_count = n_streams;
+  return TF_OK;
+}
+
+int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n, const double* boxes,
+                       const double* objectness, const float* embeddings, const uint8_t* has_embedding,
+                       const tf_records* out, const tf_trace* trace, void* cuda_stream) {
+  if (!c || !out) return fail(c, TF_ARGUMENT, "null argument");
+  if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
+  if (n < 0) return fail(c, TF_ARGUMENT, "negative detection count");
+  if (n > c->cap.max_candidates) return fail(c, TF_CAPACITY, "too many detections for max_candidates");
+  if (n > 0 && (!boxes || !objectness || !embeddings || !has_embedding))
+    return fail(c, TF_ARGUMENT, "null detection arrays");
+  int rc = check_step_config(c);
+  if (rc) return rc;
+  const long long fi = frame_index;
+  rc = check_ordering(c, stream, &fi, 1);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  TF_CUDA(c, cudaSetDevice(c->device));
+  TF_CUDA(c, cudaMemcpyAsync(c->d_frame_index, &fi, sizeof(long long), cudaMemcpyHostToDevice, st));
+  TF_CUDA(c, launch_frame_dets(boxes, objectness, embeddings, has_embedding, n, c->cap.max_candidates,
+                               c->cap.max_detections, c->det, c->P, st));
+  AssocArgs a;
+  a.det = c->det;
+  a.trk = c->trk;
+  a.trace = to_trace(trace);
+  a.frame_index = c->d_frame_index;
+  a.stream_begin = stream;
+  a.B = 1;
+  a.cap_tracks = c->cap.max_tracks;
+  a.cap_det = c->cap.max_detections;
+  a.cap_entries = c->cap_entries;
+  a.pool_col = c->pool_col;
+  a.pool_row = c->pool_row;
+  a.pool_val = c->pool_val;
+  a.out.count = out->count;
+  a.out.track_id = reinterpret_cast<long long*>(out->track_id);
+  a.out.box = out->box;
+  a.out.objectness = out->objectness;
+  a.out.max_records = out->max_records;
+  TF_CUDA(c, launch_associate(a, 1, c->P, st));
+  if (trace && trace->det_code)
+    copy_codes_kernel<<<1, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, 1, c->cap.max_detections);
+  c->last_frame[stream] = fi;
+  c->last_begin = stream;
+  c->last_count = 1;
+  return TF_OK;
+}
+
+int tf_finish(tf_ctx* c, void* cuda_stream) {
+  if (!c) return TF_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  TF_CUDA(c, cudaStreamSynchronize(st));
+  if (c->last_count == 0) return TF_OK;
+  std::vector<int> status(c->last_count);
+  TF_CUDA(c, cudaMemcpy(status.data(), c->trk.status + c->last_begin, sizeof(int) * c->last_count,
+                        cudaMemcpyDeviceToHost));
+  for (int i = 0; i < c->last_count; ++i) {
+    if (status[i] != 0) {
+      const int code = status[i] & 0xff, frame = status[i] >> 8;
+      return fail(c, code, std::string(tf_status_name(code)) + " in stream " + std::to_string(c->last_begin + i) +
+                               " at batch frame " + std::to_string(frame));
+    }
+  }
+  return TF_OK;
+}
+
+int tf_export_tracks(tf_ctx* c, int32_t stream, tf_track_export* o, void* cuda_stream) {
+  if (!c || !o) return TF_ARGUMENT;
+  if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  TF_CUDA(c, cudaStreamSynchronize(st));
+  const long long Tm = c->cap.max_tracks, D = c->cfg.embedding_dim;
+  const long long base = stream * Tm;
+  int n = 0;
+  TF_CUDA(c, cudaMemcpy(&n, c->trk.n_tracks + stream, sizeof(int), cudaMemcpyDeviceToHost));
+  long long next = 0, last = 0;
+  TF_CUDA(c, cudaMemcpy(&next, c->trk.next_id + stream, sizeof(long long), cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(&last, c->trk.last_frame + stream, sizeof(long long), cudaMemcpyDeviceToHost));
+  o->count = n;
+  o->next_id = next;
+  o->last_frame = last;
+  if (n == 0) return TF_OK;
+  std::vector<int> slot(n);
+  std::vector<double> cov(12 * static_cast<size_t>(n));
+  TF_CUDA(c, cudaMemcpy(o->track_id, c->trk.id + base, 8 * n, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(o->state, c->trk.state + base, 4 * n, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(o->hits, c->trk.hits + base, 4 * n, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(o->lost_since, c->trk.lost + base, 8 * n, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(o->last_update_frame, c->trk.last + base, 8 * n, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(o->mean, c->trk.mean + base * 8, 64 * n, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(cov.data(), c->trk.cov + base * 12, 96 * n, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(slot.data(), c->trk.slot + base, 4 * n, cudaMemcpyDeviceToHost));
+  for (int t = 0; t < n; ++t) {
+    double* C8 = o->covariance + 64 * t;
+    for (int q = 0; q < 64; ++q) C8[q] = 0.0;
+    for (int i = 0; i < 4; ++i) {
+      C8[8 * i + i] = cov[12 * t + 3 * i];
+      C8[8 * i + i + 4] = cov[12 * t + 3 * i + 1];
+      C8[8 * (i + 4) + i] = cov[12 * t + 3 * i + 1];
+      C8[8 * (i + 4) + i + 4] = cov[12 * t + 3 * i + 2];
+    }
+    TF_CUDA(c, cudaMemcpy(o->embedding + D * t, c->trk.emb_pool + (base + slot[t]) * D, 4 * D,
+                          cudaMemcpyDeviceToHost));
+  }
+  return TF_OK;
+}
+
+int tf_set_profiling(tf_ctx* c, int32_t enabled) {
+  if (!c) return TF_ARGUMENT;
+  c->profiling = enabled;
+  c->events_used = 0;
+  return TF_OK;
+}
+
+int tf_kernel_times(tf_ctx* c, double* frame_ms, double* assoc_ms, int64_t* updates) {
+  if (!c || !frame_ms || !assoc_ms || !updates) return TF_ARGUMENT;
+  *frame_ms = 0.0;
+  *assoc_ms = 0.0;
+  *updates = static_cast<int64_t>(c->events_used / 3);
+  if (c->events_used == 0) return TF_OK;
+  TF_CUDA(c, cudaEventSynchronize(c->events[c->events_used - 1]));
+  for (size_t i = 0; i + 2 < c->events_used; i += 3) {
+    float a = 0.f, b = 0.f;
+    TF_CUDA(c, cudaEventElapsedTime(&a, c->events[i], c->events[i + 1]));
+    TF_CUDA(c, cudaEventElapsedTime(&b, c->events[i + 1], c->events[i + 2]));
+    *frame_ms += a;
+    *assoc_ms += b;
+  }
+  c->events_used = 0;
+  return TF_OK;
+}
+
+// ---- stage-level entry points -------------------------------------------
+
+int tf_nms_sets(int32_t n_sets, const int32_t* offsets, const double* boxes, const double* scores,
+                const double* thresholds, uint8_t* keep, int32_t* status, void* cuda_stream) {
+  // offsets: HOST [n_sets + 1]; payloads device.
+  if (n_sets < 0 || (n_sets > 0 && !offsets)) return TF_ARGUMENT;
+  if (n_sets == 0) return TF_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  int cap = 1;
+  for (int i = 0; i < n_sets; ++i) cap = std::max(cap, offsets[i + 1] - offsets[i]);
+  if (cap > 1024) return TF_CAPACITY;
+  int* d_off = nullptr;
+  if (cudaMallocAsync(&d_off, sizeof(int) * (n_sets + 1), st) != cudaSuccess) return TF_CUDA;
+  cudaMemcpyAsync(d_off, offsets, sizeof(int) * (n_sets + 1), cudaMemcpyHostToDevice, st);
+  cudaError_t e = launch_nms_sets(n_sets, d_off, boxes, scores, thresholds, keep, status, cap, st);
+  cudaFreeAsync(d_off, st);
+  return e == cudaSuccess ? TF_OK : TF_CUDA;
+}
+
+int tf_lap_dense(int32_t n, const int32_t* shapes, const int64_t* cost_offsets, const double* costs,
+                 const int64_t* row_offsets, int32_t* col_for_row, int32_t* status, void* cuda_stream) {
+  // shapes / cost_offsets / row_offsets: HOST; costs, col_for_row, status: device.
+  if (n < 0 || (n > 0 && (!shapes || !cost_offsets || !row_offsets))) return TF_ARGUMENT;
+  if (n == 0) return TF_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  int cap_n = 1;
+  long long stride = 1;
+  for (int i = 0; i < n; ++i) {
+    cap_n = std::max(cap_n, std::max(shapes[2 * i], shapes[2 * i + 1]));
+    stride = std::max(stride, static_cast<long long>(shapes[2 * i]) * shapes[2 * i + 1]);
+  }
+  if (cap_n > 2048) return TF_CAPACITY;
+  int* d_shapes = nullptr;
+  long long *d_coff = nullptr, *d_roff = nullptr;
+  int16_t* pcol = nullptr;
+  double* pval = nullptr;
+  int* prow = nullptr;
+  bool ok = cudaMallocAsync(&d_shapes, sizeof(int) * 2 * n, st) == cudaSuccess &&
+            cudaMallocAsync(&d_coff, sizeof(long long) * n, st) == cudaSuccess &&
+            cudaMallocAsync(&d_roff, sizeof(long long) * n, st) == cudaSuccess &&
+            cudaMallocAsync(&pcol, sizeof(int16_t) * stride * n, st) == cudaSuccess &&
+            cudaMallocAsync(&pval, sizeof(double) * stride * n, st) == cudaSuccess &&
+            cudaMallocAsync(&prow, sizeof(int) * (cap_n + 1) * static_cast<size_t>(n), st) == cudaSuccess;
+  if (!ok) return TF_CUDA;
+  cudaMemcpyAsync(d_shapes, shapes, sizeof(int) * 2 * n, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_coff, cost_offsets, sizeof(long long) * n, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_roff, row_offsets, sizeof(long long) * n, cudaMemcpyHostToDevice, st);
+  cudaError_t e = launch_lap_dense(n, d_shapes, d_coff, costs, d_roff, col_for_row, status, cap_n, pcol, pval,
+                                   prow, stride, st);
+  cudaFreeAsync(d_shapes, st);
+  cudaFreeAsync(d_coff, st);
+  cudaFreeAsync(d_roff, st);
+  cudaFreeAsync(pcol, st);
+  cudaFreeAsync(pval, st);
+  cudaFreeAsync(prow, st);
+  return e == cudaSuccess ? TF_OK : TF_CUDA;
+}
+
+int tf_kalman(int32_t op, int32_t n, const tf_config* config, const double* mean_in, const double* cov_in,
+              const double* z, double* mean_out, double* cov_out, int32_t* status, void* cuda_stream) {
+  if (!config || op < 0 || op > 3 || n < 0) return TF_ARGUMENT;
+  return launch_kalman(op, n, make_params(*config), mean_in, cov_in, z, mean_out, cov_out, status,
+                       static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
+             ? TF_OK
+             : TF_CUDA;
+}
+
+int tf_gating(int32_t n_tracks, const double* means, const double* covs, int32_t n_meas, const double* z,
+              int32_t metric, const tf_config* config, double* out, int32_t* status, void* cuda_stream) {
+  if (!config || n_tracks < 0 || n_meas < 0) return TF_ARGUMENT;
+  return launch_gating(n_tracks, means, covs, n_meas, z, metric, make_params(*config), out, status,
+                       static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
+             ? TF_OK
+             : TF_CUDA;
+}
+
+int tf_cosine_cost(int32_t nt, int32_t nd, int32_t dim, const float* te, const float* de, double* out,
+                   void* cuda_stream) {
+  if (nt < 0 || nd < 0 || dim < 1) return TF_ARGUMENT;
+  return launch_cosine_cost(nt, nd, dim, te, de, out, static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
+             ? TF_OK
+             : TF_CUDA;
+}
+
+int tf_normalize_rows(int32_t n, int32_t dim, const double* in64, const float* in32, int64_t row_stride,
+                      int32_t quantize, float* out, int32_t* status, void* cuda_stream) {
+  if (n < 0 || dim < 1 || (!in64 && !in32 && n > 0)) return TF_ARGUMENT;
+  return launch_normalize_rows(n, dim, in64, in32, row_stride, quantize, out, status,
+                               static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
+             ? TF_OK
+             : TF_CUDA;
+}
+
+int tf_quantize_binary16(int64_t n, const float* in, float* out, int32_t* status, void* cuda_stream) {
+  if (n < 0) return TF_ARGUMENT;
+  return launch_binary16(n, in, out, status, static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess ? TF_OK
+                                                                                                     : TF_CUDA;
+}
+
+int tf_smooth_embedding(int32_t n, int32_t dim, const float* old_emb, const float* new_emb, double alpha,
+                        float* out, int32_t* status, void* cuda_stream) {
+  if (n < 0 || dim < 1) return TF_ARGUMENT;
+  return launch_smooth(n, dim, old_emb, new_emb, alpha, 1.0 - alpha, out, status,
+                       static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
+             ? TF_OK
+             : TF_CUDA;
+}
+
+int tf_iou_pairs(int32_t n, const double* a, const double* b, double* out, void* cuda_stream) {
+  if (n < 0) return TF_ARGUMENT;
+  return launch_iou(n, a, b, out, static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess ? TF_OK : TF_CUDA;
+}
+
+}  // extern "C"

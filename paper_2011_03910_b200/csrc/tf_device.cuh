@@ -1,0 +1,420 @@
+// Device building blocks of the decode -> NMS -> association path (sm_100a).
+//
+// Precision policy: every value that feeds a decision
+// (confidence test, IoU > thr, gate > thr, cost > max_cost, LAP costs) is
+// computed in fp64 with the reference's operation order, so decisions match
+// the CPU reference bit for bit. The translation unit is compiled with
+// --fmad=false so no a*b+c is silently contracted into an FMA.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include "../../include/trackforge_b200.h"
+
+namespace tfd {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Host-prepared constants (tf_config + derived values computed once on the host).
+struct Params {
+  double conf_threshold;   // filter_confidence  (tf/postproc.py:61-65)
+  double conf_logit;       // logit(conf_threshold): exact logit-space pre-filter of the decode
+  double nms_iou;          // tf/postproc.py:68-89
+  double max_cost;         // tf/assoc.py:90-107
+  double gate_threshold;   // tf/assoc.py:49-57
+  double alpha, beta;      // smoothing alpha and (1.0 - alpha) as Python computes it
+  double wp, wv;           // MotionNoise weights (tf/motion.py:37-38)
+  double std_aspect, std_aspect_velocity, std_aspect_measurement;
+  int gate_metric;         // 0 mahalanobis, 1 euclidean, other -> ConfigError when used
+  int max_lost, min_hits, dim, quantize;
+};
+
+// ---------------------------------------------------------------- misc
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+__device__ __forceinline__ int n_warps() { return blockDim.x >> 5; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// Order-preserving map of a double onto uint64 (for min-reductions).
+__device__ __forceinline__ unsigned long long dkey(double d) {
+  long long b = __double_as_longlong(d + 0.0);  // canonicalise -0.0
+  return (b < 0) ? ~static_cast<unsigned long long>(b)
+                 : (static_cast<unsigned long long>(b) | 0x8000000000000000ull);
+}
+
+// Record the first error (lowest packed key) in a status word. Key packs
+// (position << 8 | code) so the earliest failing row / frame wins.
+__device__ __forceinline__ void flag_error(int* status, int position, int code) {
+  atomicMin(status, (position << 8) | code);
+}
+constexpr int STATUS_CLEAR = 0x7fffffff;
+
+// ---------------------------------------------------------------- geometry
+// iou, tf/core.py:71-80 (right = x + w, bottom = y + h, area = w * h; clamp to 1).
+__device__ __forceinline__ double iou_tlwh(double ax, double ay, double aw, double ah,
+                                           double bx, double by, double bw, double bh) {
+  double iw = fmin(ax + aw, bx + bw) - fmax(ax, bx);
+  double ih = fmin(ay + ah, by + bh) - fmax(ay, by);
+  if (iw <= 0.0 || ih <= 0.0) return 0.0;
+  double inter = iw * ih;
+  double uni = (aw * ah + bw * bh) - inter;
+  return fmin(inter / uni, 1.0);
+}
+
+// box_to_measurement, tf/core.py:83-88.
+__device__ __forceinline__ void box_to_meas(const double* b, double* m) {
+  m[0] = b[0] + b[2] / 2.0;
+  m[1] = b[1] + b[3] / 2.0;
+  m[2] = b[2] / b[3];
+  m[3] = b[3];
+}
+
+// measurement_to_box + BoundingBox validation, tf/core.py:91-97, 37-43.
+// Returns false (InvalidBoxError) on non-positive or non-finite size.
+__device__ __forceinline__ bool meas_to_box(const double* m, double* b) {
+  double cx = m[0], cy = m[1], a = m[2], h = m[3];
+  double w = a * h;
+  if (!(h > 0.0) || !(w > 0.0)) return false;
+  b[0] = cx - w / 2.0;
+  b[1] = cy - h / 2.0;
+  b[2] = w;
+  b[3] = h;
+  return isfinite(b[0]) && isfinite(b[1]) && isfinite(b[2]) && isfinite(b[3]);
+}
+
+// ---------------------------------------------------------------- Kalman (compact)
+// The reference filter (tf/motion.py) keeps an 8x8 covariance, but starting
+// from initiate()'s diagonal every predict/update only ever couples state i
+// with i+4: the filter is four independent (position, velocity) pairs and the
+// innovation covariance S is exactly diagonal. We store per axis i
+// (pp, pv, vv) = (P[i][i], P[i][i+4], P[i+4][i+4]) and reproduce each
+// reference operation with its rounding order:
+//   predict: F P F^T + diag(q) then symmetrise      (tf/motion.py:83-101)
+//   project: S_i = P_ii + r_i^2                     (tf/motion.py:103-110)
+//   update : Cholesky of diagonal S, gain = (P H^T) * (1/l) * (1/l) -- LAPACK
+//            trsm multiplies by the reciprocal diagonal -- then
+//            P - (K S) K^T and symmetrise          (tf/motion.py:112-126)
+//   gate   : sum_i ((z_i - m_i) * (1/l_i))^2 summed in order i = 0..3
+//                                                   (tf/motion.py:128-142)
+struct KF {
+  // process-noise std of axis i (position block), tf/motion.py:87-98
+  __device__ static __forceinline__ double qpos(const Params& p, int i, double h) {
+    return i == 2 ? p.std_aspect : p.wp * h;
+  }
+  __device__ static __forceinline__ double qvel(const Params& p, int i, double h) {
+    return i == 2 ? p.std_aspect_velocity : p.wv * h;
+  }
+  __device__ static __forceinline__ double rstd(const Params& p, int i, double h) {
+    return i == 2 ? p.std_aspect_measurement : p.wp * h;
+  }
+
+  // initiate, tf/motion.py:61-81. mean[8], cov[12] (per axis pp, pv, vv).
+  __device__ static __forceinline__ void initiate(const Params& p, const double* z, double* mean,
+                                                  double* cov) {
+    double h = z[3];
+    double wp2 = 2.0 * p.wp, wv10 = 10.0 * p.wv;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mean[i] = z[i];
+      mean[i + 4] = 0.0;
+      double sp = (i == 2) ? p.std_aspect : wp2 * h;
+      double sv = (i == 2) ? p.std_aspect_velocity : wv10 * h;
+      cov[3 * i + 0] = sp * sp;
+      cov[3 * i + 1] = 0.0;
+      cov[3 * i + 2] = sv * sv;
+    }
+  }
+
+  __device__ static __forceinline__ void predict(const Params& p, double* mean, double* cov) {
+    double h = mean[3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double qp = qpos(p, i, h), qv = qvel(p, i, h);
+      double pp = cov[3 * i], pv = cov[3 * i + 1], vv = cov[3 * i + 2];
+      double fpp = pp + pv;          // (F P)[i][i]
+      double fpv = pv + vv;          // (F P)[i][i+4] == (F P F^T)[i][i+4]
+      cov[3 * i + 0] = (fpp + fpv) + qp * qp;
+      cov[3 * i + 1] = fpv;
+      cov[3 * i + 2] = vv + qv * qv;
+      mean[i] = mean[i] + mean[i + 4];
+    }
+  }
+
+  // Innovation variances S_i and reciprocal Cholesky factors 1/sqrt(S_i).
+  // Returns false when S is not positive definite (NumericError).
+  __device__ static __forceinline__ bool project(const Params& p, const double* mean,
+                                                 const double* cov, double* s, double* il) {
+    double h = mean[3];
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double r = rstd(p, i, h);
+      s[i] = cov[3 * i] + r * r;
+      ok = ok && (s[i] > 0.0);
+      il[i] = 1.0 / sqrt(s[i]);
+    }
+    return ok;
+  }
+
+  __device__ static __forceinline__ double mahalanobis(const double* mean, const double* il,
+                                                       const double* z) {
+    double x0 = (z[0] - mean[0]) * il[0];
+    double x1 = (z[1] - mean[1]) * il[1];
+    double x2 = (z[2] - mean[2]) * il[2];
+    double x3 = (z[3] - mean[3]) * il[3];
+    return ((x0 * x0 + x1 * x1) + x2 * x2) + x3 * x3;
+  }
+
+  __device__ static __forceinline__ bool update(const Params& p, double* mean, double* cov,
+                                                const double* z) {
+    double s[4], il[4];
+    if (!project(p, mean, cov, s, il)) return false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double pp = cov[3 * j], pv = cov[3 * j + 1], vv = cov[3 * j + 2];
+      double kp = (pp * il[j]) * il[j];
+      double kv = (pv * il[j]) * il[j];
+      double y = z[j] - mean[j];
+      mean[j] = mean[j] + kp * y;
+      mean[j + 4] = mean[j + 4] + kv * y;
+      double ksp = kp * s[j], ksv = kv * s[j];
+      double a = pv - ksp * kv;      // [j][j+4]
+      double b = pv - ksv * kp;      // [j+4][j]
+      cov[3 * j + 0] = pp - ksp * kp;
+      cov[3 * j + 2] = vv - ksv * kv;
+      cov[3 * j + 1] = (a + b) / 2.0;
+    }
+    return true;
+  }
+};
+
+// ---------------------------------------------------------------- block NMS
+// nms, tf/postproc.py:68-89, over C <= cap candidates held in shared memory.
+// Greedy order is (-score, index); a candidate is suppressed when its IoU with
+// an earlier kept one is strictly above thr. Bitmask formulation: mask[u] has
+// bit v set when sorted[v] (v > u) overlaps sorted[u]; one warp then walks the
+// sorted order OR-ing masks of kept rows.
+//  box   [C*4] tlwh, score [C], alive [C] (filter_confidence result)
+//  keep  [C] out: 1 survivor / 0 not
+//  sorted [C] int16 scratch; mask [C * words] u64 scratch (words = ceil(cap/64))
+// Returns the number of alive candidates. All threads must call.
+__device__ inline int block_nms(int C, const double* box, const double* score, const uint8_t* alive,
+                         double thr, int16_t* sorted, unsigned long long* mask, int words,
+                         uint8_t* keep, int* sh_scratch) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) sh_scratch[0] = 0;
+  __syncthreads();
+  int my_alive = 0;
+  for (int i = tid; i < C; i += nt) {
+    keep[i] = 0;
+    if (!alive[i]) continue;
+    ++my_alive;
+    double si = score[i];
+    int r = 0;
+    for (int j = 0; j < C; ++j) {
+      if (!alive[j]) continue;
+      double sj = score[j];
+      r += (sj > si) || (sj == si && j < i);
+    }
+    sorted[r] = static_cast<int16_t>(i);
+  }
+  if (my_alive) atomicAdd(sh_scratch, my_alive);
+  __syncthreads();
+  const int na = sh_scratch[0];
+  const int nwords = (na + 63) >> 6;
+  const int lane = lane_id(), wid = warp_id(), nw = n_warps();
+  for (int u = wid; u < na; u += nw) {
+    const int iu = sorted[u];
+    const double ax = box[4 * iu], ay = box[4 * iu + 1], aw = box[4 * iu + 2], ah = box[4 * iu + 3];
+    for (int w = 0; w < nwords; ++w) {
+      unsigned lohi[2];
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        int v = w * 64 + half * 32 + lane;
+        bool hit = false;
+        if (v > u && v < na) {
+          int iv = sorted[v];
+          hit = iou_tlwh(ax, ay, aw, ah, box[4 * iv], box[4 * iv + 1], box[4 * iv + 2],
+                         box[4 * iv + 3]) > thr;
+        }
+        lohi[half] = __ballot_sync(FULL, hit);
+      }
+      if (lane == 0)
+        mask[u * words + w] = static_cast<unsigned long long>(lohi[0]) |
+                              (static_cast<unsigned long long>(lohi[1]) << 32);
+    }
+  }
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long removed = 0ull;   // lane l holds word l
+    for (int u = 0; u < na; ++u) {
+      unsigned long long word = __shfl_sync(FULL, removed, u >> 6);
+      if (!((word >> (u & 63)) & 1ull)) {
+        if (lane == 0) keep[sorted[u]] = 1;
+        if (lane < nwords) removed |= mask[u * words + lane];
+      }
+    }
+  }
+  __syncthreads();
+  return na;
+}
+
+// Block-wide ordered compaction helper: exclusive prefix of 0/1 flags over
+// n items processed in chunks of blockDim. pos[i] receives the rank of item i
+// among flagged items; returns the total. All threads must call.
+template <typename FlagFn>
+__device__ int block_rank(int n, FlagFn flag, int16_t* pos, int* sh_warp /* [33] */) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
+  int base = 0;
+  for (int c = 0; c < n; c += nt) {
+    int i = c + tid;
+    bool f = (i < n) && flag(i);
+    unsigned b = __ballot_sync(FULL, f);
+    if (lane == 0) sh_warp[wid] = __popc(b);
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < nw ? sh_warp[lane] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < nw) sh_warp[lane] = incl - v;
+      if (lane == 31) sh_warp[32] = incl;
+    }
+    __syncthreads();
+    if (i < n) pos[i] = f ? static_cast<int16_t>(base + sh_warp[wid] + __popc(b & ((1u << lane) - 1u))) : -1;
+    base += sh_warp[32];
+    __syncthreads();
+  }
+  return base;
+}
+
+// ---------------------------------------------------------------- warp LAP
+// Exact restatement of the solver behind hungarian_solve (tf/assoc.py:60-87 ->
+// scipy.optimize.linear_sum_assignment, Crouse's shortest augmenting path; see
+// oracle/lap.py) on the sentinel-padded n x n matrix, executed by ONE warp.
+// Each Dijkstra iteration scans the live columns lane-parallel and reduces the
+// minimum with scipy's tie rule (a free column wins; among equals the later
+// list position for free columns, the earlier one otherwise), so the returned
+// optimum is the one the reference gets, ties included.
+//
+// Row r < nr has its finite entries as CSR (rowptr, ecol, eval); every other
+// cell (including rows >= nr and columns >= nc) costs `sentinel`.
+struct LapScratch {
+  double *u, *v, *dist, *crow;
+  int16_t *path, *row4col, *col4row, *rem, *vrows, *vcols;
+};
+
+__device__ inline void warp_lap(int n, int nr, const int* rowptr, const int16_t* ecol, const double* eval,
+                         double sentinel, LapScratch s) {
+  const int lane = lane_id();
+  for (int j = lane; j < n; j += 32) {
+    s.u[j] = 0.0;
+    s.v[j] = 0.0;
+    s.row4col[j] = -1;
+    s.col4row[j] = -1;
+    s.crow[j] = sentinel;
+  }
+  __syncwarp();
+  for (int cur = 0; cur < n; ++cur) {
+    for (int p = lane; p < n; p += 32) s.rem[p] = static_cast<int16_t>(n - 1 - p);
+    int live = n, row = cur, nvr = 0, nvc = 0, sink = -1;
+    double min_val = 0.0;
+    bool first = true;
+    __syncwarp();
+    while (sink < 0) {
+      if (lane == 0) s.vrows[nvr] = static_cast<int16_t>(row);
+      ++nvr;
+      int e0 = 0, e1 = 0;
+      if (row < nr) {
+        e0 = rowptr[row];
+        e1 = rowptr[row + 1];
+        for (int e = e0 + lane; e < e1; e += 32) s.crow[ecol[e]] = eval[e];
+      }
+      __syncwarp();
+      const double ur = s.u[row];
+      unsigned long long best = ~0ull;
+      int best_p = -1;
+      bool best_free = false;
+      for (int p = lane; p < live; p += 32) {
+        const int j = s.rem[p];
+        const double r = ((min_val + s.crow[j]) - ur) - s.v[j];
+        double d;
+        if (first || r < s.dist[j]) {
+          s.dist[j] = r;
+          s.path[j] = static_cast<int16_t>(row);
+          d = r;
+        } else {
+          d = s.dist[j];
+        }
+        const unsigned long long k = dkey(d);
+        const bool fr = s.row4col[j] < 0;
+        if (k < best || (k == best && fr)) {
+          best = k;
+          best_p = p;
+          best_free = fr;
+        }
+      }
+      __syncwarp();
+      if (row < nr)
+        for (int e = e0 + lane; e < e1; e += 32) s.crow[ecol[e]] = sentinel;
+      // warp argmin with the tie rule
+      const unsigned hi = static_cast<unsigned>(best >> 32), lo = static_cast<unsigned>(best);
+      const unsigned mh = __reduce_min_sync(FULL, hi);
+      const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+      const bool q = best_p >= 0 && hi == mh && lo == ml;
+      const unsigned fmask = __ballot_sync(FULL, q && best_free);
+      int pw;
+      if (fmask)
+        pw = static_cast<int>(__reduce_max_sync(FULL, (q && best_free) ? static_cast<unsigned>(best_p) : 0u));
+      else
+        pw = static_cast<int>(__reduce_min_sync(FULL, q ? static_cast<unsigned>(best_p) : 0xffffffffu));
+      const int j = s.rem[pw];
+      min_val = s.dist[j];
+      if (lane == 0) s.vcols[nvc] = static_cast<int16_t>(j);
+      ++nvc;
+      const int owner = s.row4col[j];
+      if (owner < 0) sink = j; else row = owner;
+      __syncwarp();
+      if (lane == 0) s.rem[pw] = s.rem[live - 1];
+      --live;
+      first = false;
+      __syncwarp();
+    }
+    // dual update (scipy order: u[cur] first, then visited rows / columns)
+    if (lane == 0) s.u[cur] = s.u[cur] + min_val;
+    for (int q = lane + 1; q < nvr; q += 32) {
+      int r = s.vrows[q];
+      s.u[r] = s.u[r] + (min_val - s.dist[s.col4row[r]]);
+    }
+    for (int q = lane; q < nvc; q += 32) {
+      int j = s.vcols[q];
+      s.v[j] = s.v[j] - (min_val - s.dist[j]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int j = sink;
+      while (true) {
+        int i = s.path[j];
+        s.row4col[j] = static_cast<int16_t>(i);
+        int t = s.col4row[i];
+        s.col4row[i] = static_cast<int16_t>(j);
+        j = t;
+        if (i == cur) break;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace tfd

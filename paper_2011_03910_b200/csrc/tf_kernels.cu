@@ -1,0 +1,1417 @@
+// sm_100a kernels of the decode -> NMS -> association path.
+//
+//  frame_heads_kernel   one CTA per frame: YOLO-head confidence scan with
+//                       warp-ballot ordered compaction, candidate box decode,
+//                       bitmask NMS, 128-bit embedding gather + fp64 L2-norm.
+//                       (K1+K2+K3 of SURVEY.md section 2, fused: the 8 conf
+//                       planes are read once, candidates never leave SMEM.)
+//  frame_dets_kernel    same NMS / det-buffer tail for already-parsed rows
+//                       (the Tracker.step entry point).
+//  associate_kernel     one CTA per stream, persistent over the B frames of an
+//                       update: Kalman predict -> gate -> sparse fp64 cosine
+//                       cost -> exact LAP -> threshold -> Kalman update, EMA,
+//                       lifecycle, births, records (K4..K9).
+//  stage kernels        batched nms / lap / kalman / gating / cost / normalize /
+//                       binary16 / smooth / iou for the reference's module-level
+//                       functions.
+#include "tf_kernels.cuh"
+
+namespace tfd {
+
+// ============================================================================
+// Frame stage (heads)
+// ============================================================================
+
+struct ScaleDev {
+  const float* head;             // confidence planes (channels 6a+4, 6a+5)
+  long long hs_n, hs_c;
+  const float* delta;            // box deltas (channels 6a+0..3)
+  long long ds_n, ds_c;
+  const float* emb;
+  long long es_n, es_c, es_h, es_w;
+  int H, W, stride, pad;
+  float aw[4], ah[4];
+};
+
+struct FrameArgs {
+  ScaleDev sc[3];
+  double scale_inv, pad_x, pad_y;
+  int frames;
+  int cap_cand, cap_det, words;
+  DetBuf det;
+};
+
+// Shared-memory plan of frame_heads_kernel (bytes computed by frame_smem_bytes()).
+struct FramePlan {
+  int nchunks;
+  size_t off_masks, off_code, off_box, off_score, off_alive, off_sorted, off_nmask, off_keep, off_pos,
+      total;
+};
+
+__host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+
+__host__ __device__ inline FramePlan frame_plan(int total_anchors, int cap_cand, int words) {
+  FramePlan p;
+  p.nchunks = (total_anchors + 31) / 32;
+  size_t o = 0;
+  p.off_masks = o;  o = align16(o + sizeof(unsigned) * p.nchunks);
+  p.off_code = o;   o = align16(o + sizeof(int) * cap_cand);
+  p.off_box = o;    o = align16(o + sizeof(double) * 4 * cap_cand);
+  p.off_score = o;  o = align16(o + sizeof(double) * cap_cand);
+  p.off_alive = o;  o = align16(o + cap_cand);
+  p.off_sorted = o; o = align16(o + sizeof(int16_t) * cap_cand);
+  p.off_nmask = o;  o = align16(o + sizeof(unsigned long long) * cap_cand * words);
+  p.off_keep = o;   o = align16(o + cap_cand);
+  p.off_pos = o;    o = align16(o + sizeof(int16_t) * cap_cand);
+  p.total = o;
+  return p;
+}
+
+// Gather one embedding row (warp-cooperative), fp64 sum of squares, optional
+// binary16 round trip; writes the fp32 unit vector to `out` when non-null.
+// Mirrors normalize (tf/core.py:100-111) and _quantize_detection
+// (tf/pipeline.py:436-441). Returns a tf_status code (0 ok). The norm of every
+// row is checked even when `out` is null (parse_output normalises all rows).
+__device__ int gather_normalize(const float* src, long long stride, int dim, int quantize, float* out) {
+  const int lane = lane_id();
+  const bool vec = (stride == 1) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (dim % 4 == 0) &&
+                   (out == nullptr || (reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  double ss = 0.0;
+  bool finite = true;
+  if (vec) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    for (int i = lane; i < dim / 4; i += 32) {
+      float4 q = __ldg(s4 + i);
+      double a = q.x, b = q.y, c = q.z, d = q.w;
+      finite = finite && isfinite(q.x) && isfinite(q.y) && isfinite(q.z) && isfinite(q.w);
+      ss += a * a;
+      ss += b * b;
+      ss += c * c;
+      ss += d * d;
+    }
+  } else {
+    for (int i = lane; i < dim; i += 32) {
+      float x = __ldg(src + static_cast<long long>(i) * stride);
+      finite = finite && isfinite(x);
+      double a = x;
+      ss += a * a;
+    }
+  }
+  ss = warp_sum(ss);
+  finite = __all_sync(FULL, finite);
+  if (!finite) return TF_DEGENERATE_EMBEDDING;
+  const double norm = sqrt(ss);
+  if (norm < 1e-12) return TF_DEGENERATE_EMBEDDING;
+  if (!quantize) {
+    if (out == nullptr) return TF_OK;
+    if (vec) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      float4* o4 = reinterpret_cast<float4*>(out);
+      for (int i = lane; i < dim / 4; i += 32) {
+        float4 q = __ldg(s4 + i);
+        float4 r;
+        r.x = static_cast<float>(static_cast<double>(q.x) / norm);
+        r.y = static_cast<float>(static_cast<double>(q.y) / norm);
+        r.z = static_cast<float>(static_cast<double>(q.z) / norm);
+        r.w = static_cast<float>(static_cast<double>(q.w) / norm);
+        o4[i] = r;
+      }
+    } else {
+      for (int i = lane; i < dim; i += 32)
+        out[i] = static_cast<float>(static_cast<double>(__ldg(src + static_cast<long long>(i) * stride)) / norm);
+    }
+    return TF_OK;
+  }
+  // MIXED: fp32 unit vector -> binary16 (RNE) -> fp32 -> normalize again.
+  double ss2 = 0.0;
+  bool inrange = true;
+  for (int i = lane; i < dim; i += 32) {
+    float u = static_cast<float>(static_cast<double>(__ldg(src + static_cast<long long>(i) * stride)) / norm);
+    inrange = inrange && fabsf(u) <= 65504.0f;
+    double h = __half2float(__float2half_rn(u));
+    ss2 += h * h;
+  }
+  ss2 = warp_sum(ss2);
+  if (!__all_sync(FULL, inrange)) return TF_PRECISION_OVERFLOW;
+  const double n2 = sqrt(ss2);
+  if (n2 < 1e-12) return TF_DEGENERATE_EMBEDDING;
+  if (out == nullptr) return TF_OK;
+  for (int i = lane; i < dim; i += 32) {
+    float u = static_cast<float>(static_cast<double>(__ldg(src + static_cast<long long>(i) * stride)) / norm);
+    double h = __half2float(__float2half_rn(u));
+    out[i] = static_cast<float>(h / n2);
+  }
+  return TF_OK;
+}
+
+__global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.x;
+  const int tid = threadIdx.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
+
+  __shared__ const float* s_bg[12];
+  __shared__ const float* s_fg[12];
+  __shared__ int s_start[13];
+  __shared__ int s_warp[33];
+  __shared__ int s_misc[4];
+
+  if (tid < 12) {
+    int si = tid / 4, an = tid % 4;
+    const ScaleDev& sc = a.sc[si];
+    const float* base = sc.head + static_cast<long long>(f) * sc.hs_n;
+    s_bg[tid] = base + static_cast<long long>(6 * an + 4) * sc.hs_c;
+    s_fg[tid] = base + static_cast<long long>(6 * an + 5) * sc.hs_c;
+  }
+  if (tid == 0) {
+    int acc = 0;
+    for (int si = 0; si < 3; ++si)
+      for (int an = 0; an < 4; ++an) {
+        s_start[si * 4 + an] = acc;
+        acc += a.sc[si].H * a.sc[si].W;
+      }
+    s_start[12] = acc;
+    s_misc[0] = STATUS_CLEAR;
+  }
+  __syncthreads();
+  const int total = s_start[12];
+  const FramePlan plan = frame_plan(total, a.cap_cand, a.words);
+  unsigned* masks = reinterpret_cast<unsigned*>(smem + plan.off_masks);
+  int* ccode = reinterpret_cast<int*>(smem + plan.off_code);
+  double* cbox = reinterpret_cast<double*>(smem + plan.off_box);
+  double* cscore = reinterpret_cast<double*>(smem + plan.off_score);
+  uint8_t* calive = smem + plan.off_alive;
+  int16_t* csorted = reinterpret_cast<int16_t*>(smem + plan.off_sorted);
+  unsigned long long* nmask = reinterpret_cast<unsigned long long*>(smem + plan.off_nmask);
+  uint8_t* ckeep = smem + plan.off_keep;
+  int16_t* cpos = reinterpret_cast<int16_t*>(smem + plan.off_pos);
+
+  // ---- pass 1: confidence scan, one ballot mask per 32 anchors -------------
+  const int nch = plan.nchunks;
+  const int per_warp = (nch + nw - 1) / nw;
+  const int c0 = wid * per_warp, c1 = min(nch, c0 + per_warp);
+  const double lim = P.conf_logit;
+  int count = 0;
+  int pl = 0;
+  constexpr int U = 4;
+  for (int c = c0; c < c1; c += U) {
+    float bg[U], fg[U];
+    bool valid[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      int g = (c + k) * 32 + lane;
+      valid[k] = (c + k < c1) && (g < total);
+      bg[k] = 0.f;
+      fg[k] = -INFINITY;
+      if (valid[k]) {
+        while (g >= s_start[pl + 1]) ++pl;
+        int pos = g - s_start[pl];
+        bg[k] = __ldcs(s_bg[pl] + pos);
+        fg[k] = __ldcs(s_fg[pl] + pos);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (c + k >= c1) break;
+      bool keep = valid[k] && ((static_cast<double>(fg[k]) - static_cast<double>(bg[k])) >= lim);
+      unsigned m = __ballot_sync(FULL, keep);
+      if (lane == 0) masks[c + k] = m;
+      count += __popc(m);
+    }
+  }
+  if (lane == 0) s_warp[wid] = count;
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < nw ? s_warp[lane] : 0, incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane < nw) s_warp[lane] = incl - v;
+    if (lane == 31) s_warp[32] = incl;
+  }
+  __syncthreads();
+  const int C_all = s_warp[32];
+  const int C = min(C_all, a.cap_cand);
+  if (tid == 0 && C_all > a.cap_cand) flag_error(&s_misc[0], 0, TF_CAPACITY);
+
+  // ---- pass 2: ordered compaction of candidate codes -----------------------
+  {
+    int base = s_warp[wid];
+    for (int c = c0; c < c1; ++c) {
+      unsigned m = masks[c];
+      if (m == 0u) continue;
+      if ((m >> lane) & 1u) {
+        int r = base + __popc(m & ((1u << lane) - 1u));
+        if (r < C) ccode[r] = c * 32 + lane;
+      }
+      base += __popc(m);
+    }
+  }
+  __syncthreads();
+
+  // ---- candidate decode (sigmoid/exp boxes, letterbox inverse) -------------
+  for (int r = tid; r < C; r += blockDim.x) {
+    int g = ccode[r];
+    int p = 0;
+    while (g >= s_start[p + 1]) ++p;
+    const int si = p >> 2, an = p & 3;
+    const ScaleDev& sc = a.sc[si];
+    const int pos = g - s_start[p];
+    const int y = pos / sc.W, x = pos - y * sc.W;
+    const float* base = sc.head + static_cast<long long>(f) * sc.hs_n + pos;
+    const float* dbase = sc.delta + static_cast<long long>(f) * sc.ds_n + pos;
+    const double tx = __ldg(dbase + (6 * an + 0) * sc.ds_c);
+    const double ty = __ldg(dbase + (6 * an + 1) * sc.ds_c);
+    const double tw = __ldg(dbase + (6 * an + 2) * sc.ds_c);
+    const double th = __ldg(dbase + (6 * an + 3) * sc.ds_c);
+    const double xl = static_cast<double>(__ldg(base + (6 * an + 5) * sc.hs_c)) -
+                      static_cast<double>(__ldg(base + (6 * an + 4) * sc.hs_c));
+    double cx = (static_cast<double>(x) + 1.0 / (1.0 + exp(-tx))) * static_cast<double>(sc.stride);
+    double cy = (static_cast<double>(y) + 1.0 / (1.0 + exp(-ty))) * static_cast<double>(sc.stride);
+    double bw = static_cast<double>(sc.aw[an]) * exp(tw);
+    double bh = static_cast<double>(sc.ah[an]) * exp(th);
+    cx = (cx - a.pad_x) * a.scale_inv;
+    cy = (cy - a.pad_y) * a.scale_inv;
+    bw = bw * a.scale_inv;
+    bh = bh * a.scale_inv;
+    double bx = cx - bw / 2.0, by = cy - bh / 2.0;
+    cbox[4 * r + 0] = bx;
+    cbox[4 * r + 1] = by;
+    cbox[4 * r + 2] = bw;
+    cbox[4 * r + 3] = bh;
+    const double score = 1.0 / (1.0 + exp(-xl));
+    cscore[r] = score;
+    calive[r] = score >= P.conf_threshold;
+    if (!(isfinite(bx) && isfinite(by) && isfinite(bw) && isfinite(bh)) || !(bw > 0.0) || !(bh > 0.0))
+      flag_error(&s_misc[0], r + 1, TF_INVALID_BOX);
+  }
+  __syncthreads();
+
+  // ---- NMS ------------------------------------------------------------------
+  block_nms(C, cbox, cscore, calive, P.nms_iou, csorted, nmask, a.words, ckeep, &s_misc[1]);
+  const int K_all = block_rank(C, [&](int i) { return ckeep[i] != 0; }, cpos, s_warp);
+  const int K = min(K_all, a.cap_det);
+  if (tid == 0 && K_all > a.cap_det) flag_error(&s_misc[0], 0, TF_CAPACITY);
+
+  // ---- det buffer: measurement, objectness, code; embeddings -------------
+  const long long fbase = static_cast<long long>(f) * a.cap_det;
+  for (int r = tid; r < C; r += blockDim.x) {
+    int k = cpos[r];
+    if (k < 0 || k >= K) continue;
+    double m[4];
+    box_to_meas(&cbox[4 * r], m);
+    double* dm = a.det.meas + (fbase + k) * 4;
+    dm[0] = m[0]; dm[1] = m[1]; dm[2] = m[2]; dm[3] = m[3];
+    a.det.obj[fbase + k] = cscore[r];
+    a.det.code[fbase + k] = ccode[r];
+  }
+  // parse_output normalises every row (tf/postproc.py:31-33), so every
+  // candidate's norm is checked; only kept ones are written.
+  const int D = P.dim;
+  for (int r = wid; r < C; r += nw) {
+    int g = ccode[r];
+    int p = 0;
+    while (g >= s_start[p + 1]) ++p;
+    const ScaleDev& sc = a.sc[p >> 2];
+    const int pos = g - s_start[p];
+    const int y = pos / sc.W, x = pos - y * sc.W;
+    const float* src = sc.emb + static_cast<long long>(f) * sc.es_n + static_cast<long long>(y) * sc.es_h +
+                       static_cast<long long>(x) * sc.es_w;
+    int k = cpos[r];
+    float* out = (k >= 0 && k < K) ? a.det.emb + (fbase + k) * D : nullptr;
+    int st = gather_normalize(src, sc.es_c, D, P.quantize, out);
+    if (st != TF_OK && lane == 0) flag_error(&s_misc[0], r + 1, st);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.det.count[f] = K;
+    a.det.cand_count[f] = C_all;
+    int st = s_misc[0];
+    a.det.status[f] = (st == STATUS_CLEAR) ? 0 : (st & 0xff);
+  }
+}
+
+// ============================================================================
+// Frame stage (already-parsed detections, the Tracker.step entry)
+// ============================================================================
+struct RowsArgs {
+  const double* boxes;
+  const double* obj;
+  const float* emb;
+  const uint8_t* has_emb;
+  int n, cap_cand, cap_det, words;
+  DetBuf det;
+};
+
+__global__ void __launch_bounds__(512) frame_dets_kernel(RowsArgs a, Params P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, wid = warp_id(), nw = n_warps(), lane = lane_id();
+  __shared__ int s_warp[33];
+  __shared__ int s_misc[4];
+  const int f = 0;
+  const FramePlan plan = frame_plan(0, a.cap_cand, a.words);
+  double* cbox = reinterpret_cast<double*>(smem + plan.off_box);
+  double* cscore = reinterpret_cast<double*>(smem + plan.off_score);
+  uint8_t* calive = smem + plan.off_alive;
+  int16_t* csorted = reinterpret_cast<int16_t*>(smem + plan.off_sorted);
+  unsigned long long* nmask = reinterpret_cast<unsigned long long*>(smem + plan.off_nmask);
+  uint8_t* ckeep = smem + plan.off_keep;
+  int16_t* cpos = reinterpret_cast<int16_t*>(smem + plan.off_pos);
+  if (tid == 0) s_misc[0] = STATUS_CLEAR;
+  const int C = a.n;
+  for (int r = tid; r < C; r += blockDim.x) {
+    for (int q = 0; q < 4; ++q) cbox[4 * r + q] = a.boxes[4 * r + q];
+    cscore[r] = a.obj[r];
+    calive[r] = a.obj[r] >= P.conf_threshold;
+  }
+  __syncthreads();
+  block_nms(C, cbox, cscore, calive, P.nms_iou, csorted, nmask, a.words, ckeep, &s_misc[1]);
+  const int K_all = block_rank(C, [&](int i) { return ckeep[i] != 0; }, cpos, s_warp);
+  const int K = min(K_all, a.cap_det);
+  if (tid == 0 && K_all > a.cap_det) flag_error(&s_misc[0], 0, TF_CAPACITY);
+  for (int r = tid; r < C; r += blockDim.x) {
+    int k = cpos[r];
+    if (k < 0 || k >= K) continue;
+    if (!a.has_emb[r]) flag_error(&s_misc[0], r + 1, TF_DIMENSION);
+    double m[4];
+    box_to_meas(&cbox[4 * r], m);
+    double* dm = a.det.meas + static_cast<long long>(k) * 4;
+    dm[0] = m[0]; dm[1] = m[1]; dm[2] = m[2]; dm[3] = m[3];
+    a.det.obj[k] = cscore[r];
+    a.det.code[k] = r;
+  }
+  const int D = P.dim;
+  for (int r = wid; r < C; r += nw) {
+    int k = cpos[r];
+    if (k < 0 || k >= K || !a.has_emb[r]) continue;
+    const float* src = a.emb + static_cast<long long>(r) * D;
+    float* dst = a.det.emb + static_cast<long long>(k) * D;
+    for (int i = lane; i < D; i += 32) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.det.count[f] = K;
+    a.det.cand_count[f] = C;
+    int st = s_misc[0];
+    a.det.status[f] = (st == STATUS_CLEAR) ? 0 : (st & 0xff);
+  }
+}
+
+// ============================================================================
+// Association: one persistent CTA per stream over the B frames of an update.
+// ============================================================================
+
+struct AssocPlan {
+  size_t off_id, off_lost, off_last, off_mean, off_cov, off_pm, off_il, off_mcost, off_state, off_hits,
+      off_slot, off_mdet, off_rowptr, off_flag, off_npos, off_rpos, off_dm, off_dobj, off_drow, off_dpos, off_gmask,
+      off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
+      off_vr, off_vc, total;
+};
+
+__host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
+  AssocPlan p;
+  const int N = T > K ? T : K;
+  const int KW = (K + 31) / 32;
+  size_t o = 0;
+#define TF_TAKE(field, bytes) p.field = o; o = align16(o + (bytes));
+  TF_TAKE(off_id, 8 * T)
+  TF_TAKE(off_lost, 8 * T)
+  TF_TAKE(off_last, 8 * T)
+  TF_TAKE(off_mean, 8 * 8 * T)
+  TF_TAKE(off_cov, 8 * 12 * T)
+  TF_TAKE(off_pm, 8 * 4 * T)
+  TF_TAKE(off_il, 8 * 4 * T)
+  TF_TAKE(off_mcost, 8 * T)
+  TF_TAKE(off_state, 4 * T)
+  TF_TAKE(off_hits, 4 * T)
+  TF_TAKE(off_slot, 4 * T)
+  TF_TAKE(off_mdet, 4 * T)
+  TF_TAKE(off_rowptr, 4 * (T + 1))
+  TF_TAKE(off_flag, 4 * T)
+  TF_TAKE(off_npos, 2 * (T > K ? T : K))
+  TF_TAKE(off_rpos, 2 * T)
+  TF_TAKE(off_dm, 8 * 4 * K)
+  TF_TAKE(off_dobj, 8 * K)
+  TF_TAKE(off_drow, 4 * K)
+  TF_TAKE(off_dpos, 2 * K)
+  TF_TAKE(off_gmask, 4 * T * KW)
+  TF_TAKE(off_ecol, 2 * E)
+  TF_TAKE(off_erow, 2 * E)
+  TF_TAKE(off_eval, 8 * E)
+  TF_TAKE(off_u, 8 * N)
+  TF_TAKE(off_v, 8 * N)
+  TF_TAKE(off_dist, 8 * N)
+  TF_TAKE(off_crow, 8 * N)
+  TF_TAKE(off_path, 2 * N)
+  TF_TAKE(off_r4c, 2 * N)
+  TF_TAKE(off_c4r, 2 * N)
+  TF_TAKE(off_rem, 2 * N)
+  TF_TAKE(off_vr, 2 * (N + 1))
+  TF_TAKE(off_vc, 2 * (N + 1))
+#undef TF_TAKE
+  p.total = o;
+  return p;
+}
+
+__global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, Params P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int ls = blockIdx.x;                 // local stream in this update
+  const int s = a.stream_begin + ls;         // global stream id
+  const int tid = threadIdx.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
+  const int Tm = a.cap_tracks, Km = a.cap_det, D = P.dim;
+  const int KW = (Km + 31) / 32;
+  const AssocPlan pl = assoc_plan(Tm, Km, a.cap_entries);
+  int64_t* t_id = reinterpret_cast<int64_t*>(smem + pl.off_id);
+  int64_t* t_lost = reinterpret_cast<int64_t*>(smem + pl.off_lost);
+  int64_t* t_last = reinterpret_cast<int64_t*>(smem + pl.off_last);
+  double* t_mean = reinterpret_cast<double*>(smem + pl.off_mean);
+  double* t_cov = reinterpret_cast<double*>(smem + pl.off_cov);
+  double* t_pm = reinterpret_cast<double*>(smem + pl.off_pm);
+  double* t_il = reinterpret_cast<double*>(smem + pl.off_il);
+  double* t_mcost = reinterpret_cast<double*>(smem + pl.off_mcost);
+  int* t_state = reinterpret_cast<int*>(smem + pl.off_state);
+  int* t_hits = reinterpret_cast<int*>(smem + pl.off_hits);
+  int* t_slot = reinterpret_cast<int*>(smem + pl.off_slot);
+  int* t_mdet = reinterpret_cast<int*>(smem + pl.off_mdet);
+  int* rowptr = reinterpret_cast<int*>(smem + pl.off_rowptr);
+  int* t_flag = reinterpret_cast<int*>(smem + pl.off_flag);
+  int16_t* npos = reinterpret_cast<int16_t*>(smem + pl.off_npos);
+  int16_t* rpos = reinterpret_cast<int16_t*>(smem + pl.off_rpos);
+  double* d_meas = reinterpret_cast<double*>(smem + pl.off_dm);
+  double* d_obj = reinterpret_cast<double*>(smem + pl.off_dobj);
+  int* d_row = reinterpret_cast<int*>(smem + pl.off_drow);
+  int16_t* d_pos = reinterpret_cast<int16_t*>(smem + pl.off_dpos);
+  unsigned* gmask = reinterpret_cast<unsigned*>(smem + pl.off_gmask);
+  LapScratch L;
+  L.u = reinterpret_cast<double*>(smem + pl.off_u);
+  L.v = reinterpret_cast<double*>(smem + pl.off_v);
+  L.dist = reinterpret_cast<double*>(smem + pl.off_dist);
+  L.crow = reinterpret_cast<double*>(smem + pl.off_crow);
+  L.path = reinterpret_cast<int16_t*>(smem + pl.off_path);
+  L.row4col = reinterpret_cast<int16_t*>(smem + pl.off_r4c);
+  L.col4row = reinterpret_cast<int16_t*>(smem + pl.off_c4r);
+  L.rem = reinterpret_cast<int16_t*>(smem + pl.off_rem);
+  L.vrows = reinterpret_cast<int16_t*>(smem + pl.off_vr);
+  L.vcols = reinterpret_cast<int16_t*>(smem + pl.off_vc);
+
+  __shared__ int s_warp[33];
+  __shared__ int s_T, s_status, s_E, s_nfree, s_err;
+  __shared__ long long s_next;
+  __shared__ double s_amp;
+
+  // Large-E overflow: entries go to this stream's global pool.
+  int16_t* ecol = reinterpret_cast<int16_t*>(smem + pl.off_ecol);
+  int16_t* erow = reinterpret_cast<int16_t*>(smem + pl.off_erow);
+  double* eval = reinterpret_cast<double*>(smem + pl.off_eval);
+
+  TrackBuf& tb = a.trk;
+  const long long sT = static_cast<long long>(s) * Tm;
+  if (tid == 0) {
+    s_T = tb.n_tracks[s];
+    s_next = tb.next_id[s];
+    s_nfree = tb.n_free[s];
+    s_status = 0;
+  }
+  __syncthreads();
+  int T = s_T;
+  for (int t = tid; t < T; t += blockDim.x) {
+    t_id[t] = tb.id[sT + t];
+    t_lost[t] = tb.lost[sT + t];
+    t_last[t] = tb.last[sT + t];
+    t_state[t] = tb.state[sT + t];
+    t_hits[t] = tb.hits[sT + t];
+    t_slot[t] = tb.slot[sT + t];
+    for (int q = 0; q < 8; ++q) t_mean[8 * t + q] = tb.mean[(sT + t) * 8 + q];
+    for (int q = 0; q < 12; ++q) t_cov[12 * t + q] = tb.cov[(sT + t) * 12 + q];
+  }
+  __syncthreads();
+
+  for (int b = 0; b < a.B; ++b) {
+    if (s_status != 0) break;                      // stream failed earlier: stop
+    const int f = ls * a.B + b;
+    const long long fK = static_cast<long long>(f) * Km;
+    const long long frame = a.frame_index[f];
+    if (a.det.status[f] != 0) {                    // decode/NMS error of this frame
+      if (tid == 0) s_status = (b << 8) | a.det.status[f];
+      break;
+    }
+    const int K = a.det.count[f];
+    T = s_T;
+    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; }
+    for (int k = tid; k < K; k += blockDim.x) {
+      for (int q = 0; q < 4; ++q) d_meas[4 * k + q] = a.det.meas[(fK + k) * 4 + q];
+      d_obj[k] = a.det.obj[fK + k];
+      d_row[k] = -1;
+    }
+    // ---- Kalman predict for every live track (tf/tracker.py:98-99) --------
+    const bool gating = (T > 0 && K > 0);
+    for (int t = tid; t < T; t += blockDim.x) {
+      double* m = &t_mean[8 * t];
+      double* c = &t_cov[12 * t];
+      KF::predict(P, m, c);
+      t_mdet[t] = -1;
+      if (gating && P.gate_metric == 0) {
+        double sv[4];
+        if (!KF::project(P, m, c, sv, &t_il[4 * t])) flag_error(&s_err, t + 1, TF_NUMERIC);
+      }
+    }
+    if (tid == 0 && gating && P.gate_metric != 0 && P.gate_metric != 1) flag_error(&s_err, 0, TF_CONFIG);
+    __syncthreads();
+
+    // ---- gate (tf/tracker.py:109-110, tf/motion.py:128-142) ----------------
+    if (gating) {
+      for (int t = wid; t < T; t += nw) {
+        const double* m = &t_mean[8 * t];
+        const double* il = &t_il[4 * t];
+        int cnt = 0;
+        for (int k0 = 0; k0 < K; k0 += 32) {
+          const int k = k0 + lane;
+          bool fin = false;
+          if (k < K) {
+            const double* z = &d_meas[4 * k];
+            double g;
+            if (P.gate_metric == 0) {
+              g = KF::mahalanobis(m, il, z);
+            } else {
+              double dx = m[0] - z[0], dy = m[1] - z[1];
+              g = dx * dx + dy * dy;
+            }
+            fin = !(g > P.gate_threshold);
+          }
+          unsigned bm = __ballot_sync(FULL, fin);
+          if (lane == 0) gmask[t * KW + (k0 >> 5)] = bm;
+          cnt += __popc(bm);
+        }
+        if (lane == 0) t_flag[t] = cnt;
+      }
+    }
+    __syncthreads();
+    // ---- CSR of finite (un-gated) entries, row-major -----------------------
+    if (gating) {
+      if (wid == 0) {
+        int carry = 0;
+        for (int t0 = 0; t0 < T; t0 += 32) {
+          int t = t0 + lane;
+          int v = t < T ? t_flag[t] : 0, incl = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            int q = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += q;
+          }
+          if (t < T) rowptr[t] = carry + incl - v;
+          carry += __shfl_sync(FULL, incl, 31);
+        }
+        if (lane == 0) { rowptr[T] = carry; s_E = carry; }
+      }
+      __syncthreads();
+      const int E = s_E;
+      if (E > a.cap_entries) {
+        ecol = a.pool_col + static_cast<long long>(s) * Tm * Km;
+        erow = a.pool_row + static_cast<long long>(s) * Tm * Km;
+        eval = a.pool_val + static_cast<long long>(s) * Tm * Km;
+      }
+      for (int t = wid; t < T; t += nw) {
+        int pos = rowptr[t];
+        for (int w = 0; w < (K + 31) / 32; ++w) {
+          unsigned bm = gmask[t * KW + w];
+          if ((bm >> lane) & 1u) {
+            int e = pos + __popc(bm & ((1u << lane) - 1u));
+            ecol[e] = static_cast<int16_t>(w * 32 + lane);
+            erow[e] = static_cast<int16_t>(t);
+          }
+          pos += __popc(bm);
+        }
+      }
+      __syncthreads();
+      // ---- fp64 cosine cost of un-gated pairs (tf/assoc.py:34-46) ----------
+      double amp = 0.0;
+      for (int e = wid; e < E; e += nw) {
+        const int t = erow[e], k = ecol[e];
+        const float* te = a.trk.emb_pool + (sT + t_slot[t]) * static_cast<long long>(D);
+        const float* de = a.det.emb + (fK + k) * static_cast<long long>(D);
+        double acc = 0.0;
+        if ((D & 3) == 0) {
+          const float4* t4 = reinterpret_cast<const float4*>(te);
+          const float4* d4 = reinterpret_cast<const float4*>(de);
+          for (int i = lane; i < D / 4; i += 32) {
+            float4 x = t4[i], y = d4[i];
+            acc += static_cast<double>(x.x) * static_cast<double>(y.x);
+            acc += static_cast<double>(x.y) * static_cast<double>(y.y);
+            acc += static_cast<double>(x.z) * static_cast<double>(y.z);
+            acc += static_cast<double>(x.w) * static_cast<double>(y.w);
+          }
+        } else {
+          for (int i = lane; i < D; i += 32) acc += static_cast<double>(te[i]) * static_cast<double>(de[i]);
+        }
+        acc = warp_sum(acc);
+        double cval = fmin(fmax(1.0 - acc, 0.0), 2.0);
+        if (lane == 0) eval[e] = cval;
+        amp = fmax(amp, fabs(cval));
+      }
+      if (lane == 0 && E > 0) {
+        // amplitude = max |finite| (tf/assoc.py:71); non-negative, so an
+        // integer max over the bit patterns is exact.
+        atomicMax(reinterpret_cast<unsigned long long*>(&s_amp), static_cast<unsigned long long>(__double_as_longlong(amp)));
+      }
+    }
+    __syncthreads();
+    if (s_err != STATUS_CLEAR) {
+      if (tid == 0) s_status = (b << 8) | (s_err & 0xff);
+      break;
+    }
+
+    // ---- exact LAP on the sentinel-padded matrix (tf/assoc.py:60-87) -------
+    if (gating && wid == 0) {
+      const int n = T > K ? T : K;
+      const double sentinel = 2.0 * static_cast<double>(n) * fmax(s_amp, 1.0) + 1.0;
+      warp_lap(n, T, rowptr, ecol, eval, sentinel, L);
+    }
+    __syncthreads();
+    // ---- matches + max_cost threshold (tf/assoc.py:77-107) -----------------
+    if (gating) {
+      for (int t = tid; t < T; t += blockDim.x) {
+        const int c = L.col4row[t];
+        int md = -1;
+        double mc = 0.0;
+        if (c < K) {
+          for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
+            if (ecol[e] == c) {
+              mc = eval[e];
+              md = (mc > P.max_cost) ? -1 : c;
+              break;
+            }
+        }
+        t_mdet[t] = md;
+        t_mcost[t] = mc;
+        if (md >= 0) d_row[md] = t;
+      }
+    }
+    __syncthreads();
+
+    // ---- matched: Kalman update + lifecycle (tf/tracker.py:114-125) --------
+    for (int t = tid; t < T; t += blockDim.x) {
+      const int k = t_mdet[t];
+      int remove = 0;
+      if (k >= 0) {
+        if (!KF::update(P, &t_mean[8 * t], &t_cov[12 * t], &d_meas[4 * k]))
+          flag_error(&s_err, t + 1, TF_NUMERIC);
+        t_state[t] = 0;
+        t_lost[t] = -1;
+        t_last[t] = frame;
+        t_hits[t] += 1;
+      } else {
+        if (t_state[t] == 0) {                    // ACTIVE -> LOST (tf/tracker.py:127-131)
+          t_state[t] = 1;
+          t_lost[t] = frame;
+        }
+        remove = (t_state[t] == 1) && (frame - t_lost[t] >= P.max_lost);   // tf/tracker.py:133-143
+      }
+      t_flag[t] = remove;
+    }
+    // EMA appearance update, one warp per matched track (tf/tracker.py:67-71, 117-119)
+    for (int t = wid; t < T; t += nw) {
+      const int k = t_mdet[t];
+      if (k < 0) continue;
+      float* te = a.trk.emb_pool + (sT + t_slot[t]) * static_cast<long long>(D);
+      const float* de = a.det.emb + (fK + k) * static_cast<long long>(D);
+      double ss = 0.0;
+      for (int i = lane; i < D; i += 32) {
+        double v = P.alpha * static_cast<double>(te[i]) + P.beta * static_cast<double>(de[i]);
+        ss += v * v;
+      }
+      ss = warp_sum(ss);
+      double nrm = sqrt(ss);
+      if (!(nrm >= 1e-12) || !isfinite(nrm)) {
+        if (lane == 0) flag_error(&s_err, t + 1, TF_DEGENERATE_EMBEDDING);
+        continue;
+      }
+      for (int i = lane; i < D; i += 32) {
+        double v = P.alpha * static_cast<double>(te[i]) + P.beta * static_cast<double>(de[i]);
+        te[i] = static_cast<float>(v / nrm);
+      }
+    }
+    __syncthreads();
+
+    // ---- records: matched tracks in list (= id) order, then births ---------
+    // Births are unmatched detections in ascending order (tf/tracker.py:145-157).
+    const int n_rec_matched = block_rank(T, [&](int t) { return t_mdet[t] >= 0 && t_hits[t] >= P.min_hits; },
+                                         npos, s_warp);
+    const long long fR = static_cast<long long>(f) * a.out.max_records;
+    for (int t = tid; t < T; t += blockDim.x) {
+      const int r = npos[t];
+      const int k = t_mdet[t];
+      if (k >= 0 && a.trace.det_track) {
+        a.trace.det_track[fK + k] = t_id[t];
+        a.trace.det_cost[fK + k] = t_mcost[t];
+        a.trace.det_matched[fK + k] = 1;
+      }
+      if (r < 0) continue;
+      double box[4];
+      if (!meas_to_box(&t_mean[8 * t], box)) flag_error(&s_err, t + 1, TF_INVALID_BOX);
+      if (r < a.out.max_records) {
+        a.out.track_id[fR + r] = t_id[t];
+        for (int q = 0; q < 4; ++q) a.out.box[(fR + r) * 4 + q] = box[q];
+        a.out.objectness[fR + r] = d_obj[k];
+      }
+    }
+    const int n_birth = block_rank(K, [&](int k) { return d_row[k] < 0; }, d_pos, s_warp);
+    // removed tracks, ranked in list order: their embedding slots are pushed
+    // onto the free stack (tf/tracker.py:133-143 keeps survivors in order)
+    const int n_rm = block_rank(T, [&](int t) { return t_flag[t] != 0; }, rpos, s_warp);
+    const int n_surv = T - n_rm;
+    if (n_surv + n_birth > Tm) {
+      if (tid == 0) s_status = (b << 8) | TF_CAPACITY;
+      break;
+    }
+    const int base_free = s_nfree;
+    for (int t = tid; t < T; t += blockDim.x)
+      if (t_flag[t]) a.trk.free_stack[sT + base_free + rpos[t]] = t_slot[t];
+    block_rank(T, [&](int t) { return t_flag[t] == 0; }, npos, s_warp);
+    // ordered in-place compaction, one chunk of blockDim rows per round:
+    // destinations never exceed sources, and a round's reads finish before
+    // its writes, so later rounds' sources are untouched.
+    for (int c0 = 0; c0 < T; c0 += blockDim.x) {
+      const int t = c0 + tid;
+      const bool mv = t < T && t_flag[t] == 0 && npos[t] != t;
+      const int d = mv ? npos[t] : -1;
+      long long r_id = 0, r_lost = 0, r_last = 0;
+      int r_state = 0, r_hits = 0, r_slot = 0;
+      double r_mean[8], r_cov[12];
+      if (mv) {
+        r_id = t_id[t]; r_lost = t_lost[t]; r_last = t_last[t];
+        r_state = t_state[t]; r_hits = t_hits[t]; r_slot = t_slot[t];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) r_mean[z] = t_mean[8 * t + z];
+#pragma unroll
+        for (int z = 0; z < 12; ++z) r_cov[z] = t_cov[12 * t + z];
+      }
+      __syncthreads();
+      if (mv) {
+        t_id[d] = r_id; t_lost[d] = r_lost; t_last[d] = r_last;
+        t_state[d] = r_state; t_hits[d] = r_hits; t_slot[d] = r_slot;
+#pragma unroll
+        for (int z = 0; z < 8; ++z) t_mean[8 * d + z] = r_mean[z];
+#pragma unroll
+        for (int z = 0; z < 12; ++z) t_cov[12 * d + z] = r_cov[z];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) s_nfree = base_free + n_rm;
+    __syncthreads();
+    // births: new tracks appended in ascending detection order
+    {
+      const int nf = s_nfree;
+      const long long next = s_next;
+      for (int k = tid; k < K; k += blockDim.x) {
+        const int r = d_pos[k];
+        if (r < 0) continue;
+        const int t = n_surv + r;
+        const double* z = &d_meas[4 * k];
+        if (!(z[3] > 0.0)) flag_error(&s_err, k + 1, TF_INVALID_MEASUREMENT);
+        KF::initiate(P, z, &t_mean[8 * t], &t_cov[12 * t]);
+        t_id[t] = next + r;
+        t_state[t] = 0;
+        t_hits[t] = 1;
+        t_lost[t] = -1;
+        t_last[t] = frame;
+        t_slot[t] = a.trk.free_stack[sT + nf - 1 - r];      // pop in birth order
+        if (a.trace.det_track) {
+          a.trace.det_track[fK + k] = next + r;
+          a.trace.det_cost[fK + k] = nan("");
+          a.trace.det_matched[fK + k] = 0;
+        }
+        if (1 >= P.min_hits) {
+          const int rr = n_rec_matched + r;
+          double box[4];
+          if (!meas_to_box(z, box)) flag_error(&s_err, k + 1, TF_INVALID_BOX);
+          if (rr < a.out.max_records) {
+            a.out.track_id[fR + rr] = next + r;
+            for (int q = 0; q < 4; ++q) a.out.box[(fR + rr) * 4 + q] = box[q];
+            a.out.objectness[fR + rr] = d_obj[k];
+          }
+        }
+      }
+      __syncthreads();
+      // copy detection embeddings into the new tracks' slots (warp per birth)
+      for (int k = wid; k < K; k += nw) {
+        const int r = d_pos[k];
+        if (r < 0) continue;
+        float* dst = a.trk.emb_pool + (sT + t_slot[n_surv + r]) * static_cast<long long>(D);
+        const float* src = a.det.emb + (fK + k) * static_cast<long long>(D);
+        for (int i = lane; i < D; i += 32) dst[i] = src[i];
+      }
+      if (tid == 0) {
+        s_nfree = nf - n_birth;
+        s_next = next + n_birth;
+        s_T = n_surv + n_birth;
+        const int nrec = n_rec_matched + (1 >= P.min_hits ? n_birth : 0);
+        a.out.count[f] = nrec;
+        if (nrec > a.out.max_records) flag_error(&s_err, 0, TF_CAPACITY);
+        if (a.trace.det_count) a.trace.det_count[f] = K;
+        if (a.trace.cand_count) a.trace.cand_count[f] = a.det.cand_count[f];
+        tb.last_frame[s] = frame;
+      }
+    }
+    __syncthreads();
+    if (s_err != STATUS_CLEAR) {
+      if (tid == 0) s_status = (b << 8) | (s_err & 0xff);
+      break;
+    }
+  }
+  __syncthreads();
+  // ---- write the stream's state back -----------------------------------------
+  T = s_T;
+  for (int t = tid; t < T; t += blockDim.x) {
+    tb.id[sT + t] = t_id[t];
+    tb.lost[sT + t] = t_lost[t];
+    tb.last[sT + t] = t_last[t];
+    tb.state[sT + t] = t_state[t];
+    tb.hits[sT + t] = t_hits[t];
+    tb.slot[sT + t] = t_slot[t];
+    for (int q = 0; q < 8; ++q) tb.mean[(sT + t) * 8 + q] = t_mean[8 * t + q];
+    for (int q = 0; q < 12; ++q) tb.cov[(sT + t) * 12 + q] = t_cov[12 * t + q];
+  }
+  if (tid == 0) {
+    tb.n_tracks[s] = T;
+    tb.next_id[s] = s_next;
+    tb.n_free[s] = s_nfree;
+    tb.status[s] = s_status;
+  }
+}
+
+// ============================================================================
+// Stage-level kernels (module functions of the reference)
+// ============================================================================
+
+__global__ void nms_sets_kernel(const int* offsets, const double* boxes, const double* scores,
+                                const double* thr, uint8_t* keep, int* status, int cap, int words) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_misc[2];
+  const int set = blockIdx.x;
+  const int o0 = offsets[set], C = offsets[set + 1] - o0;
+  if (C > cap) {
+    if (threadIdx.x == 0) status[set] = TF_CAPACITY;
+    return;
+  }
+  const FramePlan plan = frame_plan(0, cap, words);
+  double* cbox = reinterpret_cast<double*>(smem + plan.off_box);
+  double* cscore = reinterpret_cast<double*>(smem + plan.off_score);
+  uint8_t* calive = smem + plan.off_alive;
+  int16_t* csorted = reinterpret_cast<int16_t*>(smem + plan.off_sorted);
+  unsigned long long* nmask = reinterpret_cast<unsigned long long*>(smem + plan.off_nmask);
+  uint8_t* ckeep = smem + plan.off_keep;
+  for (int r = threadIdx.x; r < C; r += blockDim.x) {
+    for (int q = 0; q < 4; ++q) cbox[4 * r + q] = boxes[4 * (o0 + r) + q];
+    cscore[r] = scores[o0 + r];
+    calive[r] = 1;
+  }
+  __syncthreads();
+  block_nms(C, cbox, cscore, calive, thr[set], csorted, nmask, words, ckeep, s_misc);
+  for (int r = threadIdx.x; r < C; r += blockDim.x) keep[o0 + r] = ckeep[r];
+  if (threadIdx.x == 0) status[set] = 0;
+}
+
+__global__ void lap_dense_kernel(const int* shapes, const long long* cost_off, const double* costs,
+                                 const long long* row_off, int* col_for_row, int* status, int cap_n,
+                                 int16_t* pool_col, double* pool_val, int* pool_rowptr, long long pool_stride) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int m = blockIdx.x, lane = threadIdx.x;
+  const int nr = shapes[2 * m], nc = shapes[2 * m + 1];
+  const double* c = costs + cost_off[m];
+  int* out = col_for_row + row_off[m];
+  const int n = nr > nc ? nr : nc;
+  if (nr == 0 || nc == 0) {
+    for (int r = lane; r < nr; r += 32) out[r] = -1;
+    if (lane == 0) status[m] = 0;
+    return;
+  }
+  if (n > cap_n) {
+    if (lane == 0) status[m] = TF_CAPACITY;
+    return;
+  }
+  // CSR of finite entries (global pool slice of this matrix) + amplitude
+  int16_t* ecol = pool_col + m * pool_stride;
+  double* eval = pool_val + m * pool_stride;
+  int* rowptr = pool_rowptr + static_cast<long long>(m) * (cap_n + 1);
+  double amp = 0.0;
+  bool any = false;
+  int carry = 0;
+  for (int r = 0; r < nr; ++r) {
+    if (lane == 0) rowptr[r] = carry;
+    for (int k0 = 0; k0 < nc; k0 += 32) {
+      int k = k0 + lane;
+      double v = k < nc ? c[static_cast<long long>(r) * nc + k] : INFINITY;
+      bool fin = isfinite(v);
+      unsigned bm = __ballot_sync(FULL, fin);
+      if (fin) {
+        int e = carry + __popc(bm & ((1u << lane) - 1u));
+        ecol[e] = static_cast<int16_t>(k);
+        eval[e] = v;
+        amp = fmax(amp, fabs(v));
+        any = true;
+      }
+      carry += __popc(bm);
+    }
+  }
+  if (lane == 0) rowptr[nr] = carry;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amp = fmax(amp, __shfl_xor_sync(FULL, amp, o));
+  any = __any_sync(FULL, any);
+  __syncwarp();
+  const double sentinel = 2.0 * static_cast<double>(n) * fmax(any ? amp : 1.0, 1.0) + 1.0;
+  LapScratch L;
+  size_t o = 0;
+  L.u = reinterpret_cast<double*>(smem + o); o += 8 * n;
+  L.v = reinterpret_cast<double*>(smem + o); o += 8 * n;
+  L.dist = reinterpret_cast<double*>(smem + o); o += 8 * n;
+  L.crow = reinterpret_cast<double*>(smem + o); o += 8 * n;
+  L.path = reinterpret_cast<int16_t*>(smem + o); o += 2 * n;
+  L.row4col = reinterpret_cast<int16_t*>(smem + o); o += 2 * n;
+  L.col4row = reinterpret_cast<int16_t*>(smem + o); o += 2 * n;
+  L.rem = reinterpret_cast<int16_t*>(smem + o); o += 2 * n;
+  L.vrows = reinterpret_cast<int16_t*>(smem + o); o += 2 * (n + 1);
+  L.vcols = reinterpret_cast<int16_t*>(smem + o);
+  warp_lap(n, nr, rowptr, ecol, eval, sentinel, L);
+  __syncwarp();
+  for (int r = lane; r < nr; r += 32) {
+    int col = L.col4row[r];
+    bool fin = col < nc && isfinite(c[static_cast<long long>(r) * nc + col]);
+    out[r] = fin ? col : -1;
+  }
+  if (lane == 0) status[m] = 0;
+}
+
+// Dense 8x8 Kalman (KalmanFilter API on arbitrary states). Follows the matrix
+// expressions of tf/motion.py term by term; on block-structured inputs (every
+// state the tracker produces) it reproduces the compact form bit for bit.
+__device__ void mm8(const double* A, const double* B, double* C, bool bt) {
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      double acc = 0.0;
+      for (int k = 0; k < 8; ++k) acc = acc + A[8 * i + k] * (bt ? B[8 * j + k] : B[8 * k + j]);
+      C[8 * i + j] = acc;
+    }
+}
+
+__global__ void kalman_kernel(int op, int n, Params P, const double* mean_in, const double* cov_in,
+                              const double* zin, double* mean_out, double* cov_out, int* status) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double m[8], c[64], z[4];
+  if (op != 0) {
+    for (int q = 0; q < 8; ++q) m[q] = mean_in[8 * i + q];
+    for (int q = 0; q < 64; ++q) c[q] = cov_in[64 * i + q];
+  }
+  if (op == 0 || op == 3)
+    for (int q = 0; q < 4; ++q) z[q] = zin[4 * i + q];
+  int st = 0;
+  if (op == 0) {
+    double h = z[3];
+    if (!(h > 0.0)) st = TF_INVALID_MEASUREMENT;
+    double mm[8], cc[12];
+    KF::initiate(P, z, mm, cc);
+    for (int q = 0; q < 8; ++q) mean_out[8 * i + q] = mm[q];
+    for (int q = 0; q < 64; ++q) cov_out[64 * i + q] = 0.0;
+    for (int a4 = 0; a4 < 4; ++a4) {
+      cov_out[64 * i + 9 * a4] = cc[3 * a4];
+      cov_out[64 * i + 9 * (a4 + 4)] = cc[3 * a4 + 2];
+    }
+  } else if (op == 1) {
+    const double h = m[3];
+    double F[64] = {0}, FP[64], R[64];
+    for (int q = 0; q < 8; ++q) F[9 * q] = 1.0;
+    for (int q = 0; q < 4; ++q) F[8 * q + q + 4] = 1.0;
+    double mo[8];
+    for (int r = 0; r < 8; ++r) {
+      double acc = 0.0;
+      for (int k = 0; k < 8; ++k) acc = acc + F[8 * r + k] * m[k];
+      mo[r] = acc;
+    }
+    mm8(F, c, FP, false);
+    mm8(FP, F, R, true);
+    for (int q = 0; q < 4; ++q) {
+      double sp = KF::qpos(P, q, h), sv = KF::qvel(P, q, h);
+      R[9 * q] = R[9 * q] + sp * sp;
+      R[9 * (q + 4)] = R[9 * (q + 4)] + sv * sv;
+    }
+    for (int r = 0; r < 8; ++r) {
+      mean_out[8 * i + r] = mo[r];
+      for (int k = 0; k < 8; ++k) cov_out[64 * i + 8 * r + k] = (R[8 * r + k] + R[8 * k + r]) / 2.0;
+    }
+  } else if (op == 2 || op == 3) {
+    const double h = m[3];
+    double S[16], Lc[16] = {0};
+    for (int r = 0; r < 4; ++r)
+      for (int k = 0; k < 4; ++k) S[4 * r + k] = c[8 * r + k];
+    for (int q = 0; q < 4; ++q) {
+      double rs = KF::rstd(P, q, h);
+      S[5 * q] = S[5 * q] + rs * rs;
+    }
+    if (op == 2) {
+      for (int q = 0; q < 4; ++q) mean_out[4 * i + q] = m[q];
+      for (int q = 0; q < 16; ++q) cov_out[16 * i + q] = S[q];
+    } else {
+      // Cholesky (lower), diagonal reciprocal as LAPACK/OpenBLAS applies it
+      double inv[4];
+      for (int j = 0; j < 4 && !st; ++j) {
+        double acc = S[5 * j];
+        for (int k = 0; k < j; ++k) acc = acc - Lc[4 * j + k] * Lc[4 * j + k];
+        if (!(acc > 0.0)) { st = TF_NUMERIC; break; }
+        Lc[5 * j] = sqrt(acc);
+        inv[j] = 1.0 / Lc[5 * j];
+        for (int r = j + 1; r < 4; ++r) {
+          double v = S[4 * r + j];
+          for (int k = 0; k < j; ++k) v = v - Lc[4 * r + k] * Lc[4 * j + k];
+          Lc[4 * r + j] = v * inv[j];
+        }
+      }
+      if (!st) {
+        // gain^T = S^-1 (P H^T)^T via L then L^T solves, column by column
+        double G[32];   // [4][8]
+        for (int col = 0; col < 8; ++col) {
+          double y[4];
+          for (int r = 0; r < 4; ++r) {
+            double v = c[8 * col + r];        // (P H^T)^T [r][col] = P[col][r]
+            for (int k = 0; k < r; ++k) v = v - Lc[4 * r + k] * y[k];
+            y[r] = v * inv[r];
+          }
+          for (int r = 3; r >= 0; --r) {
+            double v = y[r];
+            for (int k = r + 1; k < 4; ++k) v = v - Lc[4 * k + r] * G[8 * k + col];
+            G[8 * r + col] = v * inv[r];
+          }
+        }
+        double inn[4];
+        for (int q = 0; q < 4; ++q) inn[q] = z[q] - m[q];
+        double KS[32], NC[64];
+        for (int r = 0; r < 8; ++r) {
+          double acc = 0.0;
+          for (int k = 0; k < 4; ++k) acc = acc + G[8 * k + r] * inn[k];
+          mean_out[8 * i + r] = m[r] + acc;
+          for (int k = 0; k < 4; ++k) {
+            double s2 = 0.0;
+            for (int q = 0; q < 4; ++q) s2 = s2 + G[8 * q + r] * S[4 * q + k];
+            KS[4 * r + k] = s2;
+          }
+        }
+        for (int r = 0; r < 8; ++r)
+          for (int k = 0; k < 8; ++k) {
+            double acc = 0.0;
+            for (int q = 0; q < 4; ++q) acc = acc + KS[4 * r + q] * G[8 * q + k];
+            NC[8 * r + k] = c[8 * r + k] - acc;
+          }
+        for (int r = 0; r < 8; ++r)
+          for (int k = 0; k < 8; ++k) cov_out[64 * i + 8 * r + k] = (NC[8 * r + k] + NC[8 * k + r]) / 2.0;
+      }
+    }
+  }
+  status[i] = st;
+}
+
+__global__ void gating_kernel(int nt, const double* means, const double* covs, int nm, const double* z,
+                              int metric, Params P, double* out, int* status) {
+  const int t = blockIdx.x;
+  const double* m = means + 8 * t;
+  const double* c = covs + 64 * t;
+  __shared__ double s_l[16], s_inv[4];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) {
+    s_bad = 0;
+    if (metric == 0) {
+      double S[16], Lc[16] = {0};
+      const double h = m[3];
+      for (int r = 0; r < 4; ++r)
+        for (int k = 0; k < 4; ++k) S[4 * r + k] = c[8 * r + k];
+      for (int q = 0; q < 4; ++q) {
+        double rs = KF::rstd(P, q, h);
+        S[5 * q] = S[5 * q] + rs * rs;
+      }
+      for (int j = 0; j < 4; ++j) {
+        double acc = S[5 * j];
+        for (int k = 0; k < j; ++k) acc = acc - Lc[4 * j + k] * Lc[4 * j + k];
+        if (!(acc > 0.0)) { s_bad = 1; break; }
+        Lc[5 * j] = sqrt(acc);
+        s_inv[j] = 1.0 / Lc[5 * j];
+        for (int r = j + 1; r < 4; ++r) {
+          double v = S[4 * r + j];
+          for (int k = 0; k < j; ++k) v = v - Lc[4 * r + k] * Lc[4 * j + k];
+          Lc[4 * r + j] = v * s_inv[j];
+        }
+      }
+      for (int q = 0; q < 16; ++q) s_l[q] = Lc[q];
+    } else if (metric != 1) {
+      s_bad = 2;
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) status[t] = s_bad == 1 ? TF_NUMERIC : TF_CONFIG;
+    return;
+  }
+  for (int k = threadIdx.x; k < nm; k += blockDim.x) {
+    const double* zz = z + 4 * k;
+    double g;
+    if (metric == 0) {
+      double x[4];
+      for (int r = 0; r < 4; ++r) {
+        double v = zz[r] - m[r];
+        for (int q = 0; q < r; ++q) v = v - s_l[4 * r + q] * x[q];
+        x[r] = v * s_inv[r];
+      }
+      g = ((x[0] * x[0] + x[1] * x[1]) + x[2] * x[2]) + x[3] * x[3];
+    } else {
+      double dx = m[0] - zz[0], dy = m[1] - zz[1];
+      g = dx * dx + dy * dy;
+    }
+    out[static_cast<long long>(t) * nm + k] = g;
+  }
+  if (threadIdx.x == 0) status[t] = 0;
+}
+
+__global__ void cosine_cost_kernel(int nt, int nd, int dim, const float* te, const float* de, double* out) {
+  const int pair = blockIdx.x * n_warps() + warp_id();
+  if (pair >= nt * nd) return;
+  const int t = pair / nd, k = pair % nd;
+  double acc = 0.0;
+  for (int i = lane_id(); i < dim; i += 32)
+    acc += static_cast<double>(te[static_cast<long long>(t) * dim + i]) *
+           static_cast<double>(de[static_cast<long long>(k) * dim + i]);
+  acc = warp_sum(acc);
+  if (lane_id() == 0) out[pair] = fmin(fmax(1.0 - acc, 0.0), 2.0);
+}
+
+__global__ void normalize_rows_kernel(int n, int dim, const double* in64, const float* in32, long long stride,
+                                      int quantize, float* out, int* status) {
+  const int r = blockIdx.x * n_warps() + warp_id();
+  if (r >= n) return;
+  const int lane = lane_id();
+  double ss = 0.0;
+  bool fin = true;
+  for (int i = lane; i < dim; i += 32) {
+    double v = in64 ? in64[r * stride + i] : static_cast<double>(in32[r * stride + i]);
+    fin = fin && isfinite(v);
+    ss += v * v;
+  }
+  ss = warp_sum(ss);
+  fin = __all_sync(FULL, fin);
+  double nrm = sqrt(ss);
+  int st = 0;
+  if (!fin || nrm < 1e-12) st = TF_DEGENERATE_EMBEDDING;
+  float* o = out + static_cast<long long>(r) * dim;
+  if (!st) {
+    double ss2 = 0.0;
+    bool inrange = true;
+    for (int i = lane; i < dim; i += 32) {
+      double v = in64 ? in64[r * stride + i] : static_cast<double>(in32[r * stride + i]);
+      float u = static_cast<float>(v / nrm);
+      if (quantize) {
+        inrange = inrange && fabsf(u) <= 65504.0f;
+        u = __half2float(__float2half_rn(u));
+        double d = u;
+        ss2 += d * d;
+      }
+      o[i] = u;
+    }
+    if (quantize) {
+      ss2 = warp_sum(ss2);
+      if (!__all_sync(FULL, inrange)) st = TF_PRECISION_OVERFLOW;
+      double n2 = sqrt(ss2);
+      if (!st && n2 < 1e-12) st = TF_DEGENERATE_EMBEDDING;
+      __syncwarp();
+      if (!st)
+        for (int i = lane; i < dim; i += 32) o[i] = static_cast<float>(static_cast<double>(o[i]) / n2);
+    }
+  }
+  if (lane == 0) status[r] = st;
+}
+
+__global__ void binary16_kernel(long long n, const float* in, float* out, int* status) {
+  long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float v = in[i];
+  int st = 0;
+  if (!isfinite(v) || fabsf(v) > 65504.0f) st = TF_PRECISION_OVERFLOW;
+  out[i] = __half2float(__float2half_rn(v));
+  status[i] = st;
+}
+
+__global__ void smooth_kernel(int n, int dim, const float* oldv, const float* newv, double alpha, double beta,
+                              float* out, int* status) {
+  const int r = blockIdx.x * n_warps() + warp_id();
+  if (r >= n) return;
+  const int lane = lane_id();
+  const float* o = oldv + static_cast<long long>(r) * dim;
+  const float* q = newv + static_cast<long long>(r) * dim;
+  double ss = 0.0;
+  bool fin = true;
+  for (int i = lane; i < dim; i += 32) {
+    double v = alpha * static_cast<double>(o[i]) + beta * static_cast<double>(q[i]);
+    fin = fin && isfinite(v);
+    ss += v * v;
+  }
+  ss = warp_sum(ss);
+  fin = __all_sync(FULL, fin);
+  double nrm = sqrt(ss);
+  int st = (!fin || nrm < 1e-12) ? TF_DEGENERATE_EMBEDDING : 0;
+  if (!st)
+    for (int i = lane; i < dim; i += 32) {
+      double v = alpha * static_cast<double>(o[i]) + beta * static_cast<double>(q[i]);
+      out[static_cast<long long>(r) * dim + i] = static_cast<float>(v / nrm);
+    }
+  if (lane == 0) status[r] = st;
+}
+
+__global__ void iou_kernel(int n, const double* a, const double* b, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = iou_tlwh(a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3], b[4 * i], b[4 * i + 1], b[4 * i + 2],
+                    b[4 * i + 3]);
+}
+
+// ============================================================================
+// Host launchers
+// ============================================================================
+
+size_t frame_smem_bytes(int total_anchors, int cap_cand) {
+  return frame_plan(total_anchors, cap_cand, (cap_cand + 63) / 64).total;
+}
+size_t assoc_smem_bytes(int cap_tracks, int cap_det, int cap_entries) {
+  return assoc_plan(cap_tracks, cap_det, cap_entries).total;
+}
+
+cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_t st) {
+  FrameArgs a;
+  for (int i = 0; i < 3; ++i) {
+    const tf_head_scale& s = h.heads->scale[i];
+    a.sc[i].head = h.head_ptr[i];
+    a.sc[i].hs_n = s.head_stride_n;
+    a.sc[i].hs_c = s.head_stride_c;
+    a.sc[i].delta = h.delta_ptr[i];
+    a.sc[i].ds_n = h.delta_stride_n[i];
+    a.sc[i].ds_c = h.delta_stride_c[i];
+    a.sc[i].emb = h.emb_ptr[i];
+    a.sc[i].es_n = s.emb_stride_n;
+    a.sc[i].es_c = s.emb_stride_c;
+    a.sc[i].es_h = s.emb_stride_h;
+    a.sc[i].es_w = s.emb_stride_w;
+    a.sc[i].H = s.height;
+    a.sc[i].W = s.width;
+    a.sc[i].stride = s.stride;
+    a.sc[i].pad = 0;
+    for (int q = 0; q < 4; ++q) {
+      a.sc[i].aw[q] = s.anchors[2 * q];
+      a.sc[i].ah[q] = s.anchors[2 * q + 1];
+    }
+  }
+  a.scale_inv = h.heads->scale_inv;
+  a.pad_x = h.heads->pad_x;
+  a.pad_y = h.heads->pad_y;
+  a.frames = h.frames;
+  a.cap_cand = h.cap_cand;
+  a.cap_det = h.cap_det;
+  a.words = (h.cap_cand + 63) / 64;
+  a.det = h.det;
+  int total = 0;
+  for (int i = 0; i < 3; ++i) total += 4 * h.heads->scale[i].height * h.heads->scale[i].width;
+  const size_t smem = frame_smem_bytes(total, h.cap_cand);
+  cudaFuncSetAttribute(frame_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  frame_heads_kernel<<<h.frames, 512, smem, st>>>(a, P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frame_dets(const double* boxes, const double* obj, const float* emb, const uint8_t* has,
+                              int n, int cap_cand, int cap_det, const DetBuf& det, const Params& P,
+                              cudaStream_t st) {
+  RowsArgs a;
+  a.boxes = boxes;
+  a.obj = obj;
+  a.emb = emb;
+  a.has_emb = has;
+  a.n = n;
+  a.cap_cand = cap_cand;
+  a.cap_det = cap_det;
+  a.words = (cap_cand + 63) / 64;
+  a.det = det;
+  const size_t smem = frame_smem_bytes(0, cap_cand);
+  cudaFuncSetAttribute(frame_dets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  frame_dets_kernel<<<1, 512, smem, st>>>(a, P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st) {
+  const size_t smem = assoc_smem_bytes(a.cap_tracks, a.cap_det, a.cap_entries);
+  cudaFuncSetAttribute(associate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  associate_kernel<<<n_streams, kAssocThreads, smem, st>>>(a, P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nms_sets(int n_sets, const int* offsets, const double* boxes, const double* scores,
+                            const double* thr, uint8_t* keep, int* status, int cap, cudaStream_t st) {
+  const int words = (cap + 63) / 64;
+  const size_t smem = frame_smem_bytes(0, cap);
+  cudaFuncSetAttribute(nms_sets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  nms_sets_kernel<<<n_sets, 256, smem, st>>>(offsets, boxes, scores, thr, keep, status, cap, words);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lap_dense(int n, const int* shapes, const long long* cost_off, const double* costs,
+                             const long long* row_off, int* col_for_row, int* status, int cap_n,
+                             int16_t* pool_col, double* pool_val, int* pool_rowptr, long long pool_stride,
+                             cudaStream_t st) {
+  const size_t smem = 32 * static_cast<size_t>(cap_n) + 12 * static_cast<size_t>(cap_n) + 64;
+  cudaFuncSetAttribute(lap_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  lap_dense_kernel<<<n, 32, smem, st>>>(shapes, cost_off, costs, row_off, col_for_row, status, cap_n, pool_col,
+                                        pool_val, pool_rowptr, pool_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kalman(int op, int n, const Params& P, const double* mi, const double* ci, const double* z,
+                          double* mo, double* co, int* status, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  kalman_kernel<<<(n + 63) / 64, 64, 0, st>>>(op, n, P, mi, ci, z, mo, co, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gating(int nt, const double* means, const double* covs, int nm, const double* z, int metric,
+                          const Params& P, double* out, int* status, cudaStream_t st) {
+  if (nt == 0) return cudaSuccess;
+  gating_kernel<<<nt, 128, 0, st>>>(nt, means, covs, nm, z, metric, P, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cosine_cost(int nt, int nd, int dim, const float* te, const float* de, double* out,
+                               cudaStream_t st) {
+  const int pairs = nt * nd;
+  if (pairs == 0) return cudaSuccess;
+  cosine_cost_kernel<<<(pairs + 7) / 8, 256, 0, st>>>(nt, nd, dim, te, de, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_normalize_rows(int n, int dim, const double* in64, const float* in32, long long stride,
+                                  int quantize, float* out, int* status, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  normalize_rows_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, dim, in64, in32, stride, quantize, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_binary16(long long n, const float* in, float* out, int* status, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  binary16_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, in, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_smooth(int n, int dim, const float* o, const float* q, double alpha, double beta, float* out,
+                          int* status, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  smooth_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, dim, o, q, alpha, beta, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_iou(int n, const double* a, const double* b, double* out, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  iou_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, a, b, out);
+  return cudaGetLastError();
+}
+
+}  // namespace tfd

@@ -1,0 +1,180 @@
+"""Batched ``update(head_outputs) -> online_tracks`` over S streams x B frames.
+
+This is the north-star entry point: the JDE/YOLO head tensors of a batch go
+in (device tensors, or pinned host tensors for the end-to-end path), and the
+per-frame online tracks come out, with per-frame semantics identical to
+``parse_output`` + ``Tracker.step`` of the reference (tf/postproc.py:19-42,
+tf/tracker.py:85-159, call site tf/pipeline.py:291-302).
+
+Head layout (see oracle/heads.py for the pinned decode semantics):
+  head[i]  [S*B, 24, H_i, W_i] fp32, channel 6a+k (k: tx, ty, tw, th, bg, fg)
+  emb[i]   [S*B, D, H_i, W_i]  fp32, any strides (channels_last is the fast path)
+with scales in candidate order (stride 32, 16, 8) and frames stream-major.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .engine import Capacity, Engine
+from .errors import LayoutError
+from .tracker import TrackerConfig, records_from_device
+
+INPUT_W, INPUT_H = 1088, 608
+IMAGE_W, IMAGE_H = 1920, 1080
+STRIDES = (32, 16, 8)
+GRID = {32: (19, 34), 16: (38, 68), 8: (76, 136)}
+ANCHORS = {
+    8: ((8.0, 24.0), (11.0, 34.0), (16.0, 48.0), (23.0, 68.0)),
+    16: ((32.0, 96.0), (45.0, 135.0), (64.0, 192.0), (90.0, 271.0)),
+    32: ((128.0, 384.0), (180.0, 540.0), (256.0, 640.0), (512.0, 640.0)),
+}
+TOTAL_ANCHORS = sum(4 * h * w for h, w in GRID.values())   # 54,264
+N_CELLS = sum(h * w for h, w in GRID.values())             # 13,566
+
+
+def letterbox() -> tuple[float, float, float]:
+    """(scale_inv, pad_x, pad_y) of the JDE letterbox 1920x1080 -> 1088x608."""
+    ratio = min(INPUT_W / IMAGE_W, INPUT_H / IMAGE_H)
+    new_w, new_h = round(IMAGE_W * ratio), round(IMAGE_H * ratio)
+    return IMAGE_H / INPUT_H, (INPUT_W - new_w) / 2.0, (INPUT_H - new_h) / 2.0
+
+
+@dataclass
+class HeadOutputs:
+    """Network outputs of one batch: three head tensors and three embedding maps."""
+
+    heads: tuple   # 3 x torch.Tensor [N, 24, H, W]
+    embs: tuple    # 3 x torch.Tensor [N, D, H, W]
+
+    @property
+    def frames(self) -> int:
+        return int(self.heads[0].shape[0])
+
+
+@dataclass
+class OnlineTracks:
+    """Per-frame records of one update; device tensors plus host accessors."""
+
+    count: object        # [F] int32
+    track_id: object     # [F, R] int64
+    box: object          # [F, R, 4] float64 tlwh
+    objectness: object   # [F, R] float64
+    frame_index: np.ndarray
+    B: int
+
+    def records(self, stream: int, b: int):
+        f = stream * self.B + b
+        n = int(self.count[f])
+        return records_from_device(n, np.asarray(self.track_id[f, :n].cpu() if hasattr(self.track_id, "cpu")
+                                                 else self.track_id[f, :n]),
+                                   np.asarray(self.box[f, :n].cpu() if hasattr(self.box, "cpu") else self.box[f, :n]),
+                                   np.asarray(self.objectness[f, :n].cpu() if hasattr(self.objectness, "cpu")
+                                              else self.objectness[f, :n]))
+
+
+def _scale_desc(head, emb, stride: int) -> _lib.TfHeadScale:
+    h, w = GRID[stride]
+    if tuple(head.shape[1:]) != (24, h, w):
+        raise LayoutError(f"head of stride {stride} must be [N, 24, {h}, {w}], got {tuple(head.shape)}")
+    if tuple(emb.shape[2:]) != (h, w) or emb.shape[0] != head.shape[0]:
+        raise LayoutError(f"embedding map of stride {stride} must be [N, D, {h}, {w}], got {tuple(emb.shape)}")
+    hs = head.stride()
+    if hs[3] != 1 or hs[2] != w or head.dtype.itemsize != 4 or emb.dtype.itemsize != 4:
+        raise LayoutError("head planes must be fp32 with contiguous H*W planes")
+    es = emb.stride()
+    d = _lib.TfHeadScale(head=head.data_ptr(), head_stride_n=hs[0], head_stride_c=hs[1], emb=emb.data_ptr(),
+                         emb_stride_n=es[0], emb_stride_c=es[1], emb_stride_h=es[2], emb_stride_w=es[3],
+                         height=h, width=w, stride=stride, reserved=0)
+    for a, (aw, ah) in enumerate(ANCHORS[stride]):
+        d.anchors[2 * a] = aw
+        d.anchors[2 * a + 1] = ah
+    return d
+
+
+def heads_descriptor(out: HeadOutputs, host_memory: bool) -> _lib.TfHeads:
+    desc = _lib.TfHeads()
+    for i, s in enumerate(STRIDES):
+        desc.scale[i] = _scale_desc(out.heads[i], out.embs[i], s)
+    desc.scale_inv, desc.pad_x, desc.pad_y = letterbox()
+    desc.host_memory = int(host_memory)
+    return desc
+
+
+class BatchTracker:
+    """S independent trackers updated with B frames each per call."""
+
+    def __init__(self, num_streams: int, config: TrackerConfig | None = None, *, frames_per_update: int = 8,
+                 capacity: Capacity | None = None, quantize: bool = False):
+        self.config = config or TrackerConfig()
+        self.S = int(num_streams)
+        cap = capacity or Capacity(streams=self.S, max_frames=self.S * frames_per_update)
+        if cap.streams < self.S:
+            raise ValueError("capacity.streams < num_streams")
+        self.engine = Engine(self.config, cap, quantize=quantize)
+        self.frame = np.full(self.S, -1, np.int64)
+
+    def _frames(self, n_streams: int, B: int, frame_index) -> np.ndarray:
+        if frame_index is None:
+            return (self.frame[:n_streams, None] + 1 + np.arange(B)[None, :]).astype(np.int64).reshape(-1)
+        return np.ascontiguousarray(frame_index, dtype=np.int64).reshape(-1)
+
+    def update(self, head_outputs: HeadOutputs, frame_index=None, *, stream_begin: int = 0,
+               n_streams: int | None = None, trace: bool = False, sync: bool = True,
+               host_out: dict | None = None) -> OnlineTracks:
+        """Run decode + NMS + association for ``n_streams`` streams x B frames.
+
+        Device tensors by default; pinned host tensors (``tensor.is_pinned()``)
+        select the end-to-end path, whose records land in ``host_out`` (dict of
+        pinned host tensors from :meth:`host_output`)."""
+        eng = self.engine
+        n_streams = self.S if n_streams is None else n_streams
+        F = head_outputs.frames
+        if F % n_streams:
+            raise LayoutError(f"{F} frames do not split over {n_streams} streams")
+        B = F // n_streams
+        host = not head_outputs.heads[0].is_cuda
+        if host and not all(t.is_pinned() for t in (*head_outputs.heads, *head_outputs.embs)):
+            raise LayoutError("host inputs must be pinned (torch.Tensor.pin_memory())")
+        frames = self._frames(n_streams, B, frame_index)
+        desc = heads_descriptor(head_outputs, host)
+        if host:
+            if host_out is None:
+                host_out = self.host_output(F)
+            rec = _lib.TfRecords(host_out["count"].data_ptr(), host_out["track_id"].data_ptr(),
+                                 host_out["box"].data_ptr(), host_out["objectness"].data_ptr(),
+                                 eng.cap.max_detections, 0)
+        else:
+            rec = eng.records
+        code = eng.lib.tf_update_heads(eng.ctx, C.byref(desc), stream_begin, n_streams, B, frames.ctypes.data,
+                                       C.byref(rec), C.byref(eng.trace) if trace else None,
+                                       _lib.stream_handle())
+        eng.check(code, "update")
+        if sync:
+            eng.finish()
+        self.frame[stream_begin:stream_begin + n_streams] = frames.reshape(n_streams, B)[:, -1]
+        if host:
+            return OnlineTracks(host_out["count"], host_out["track_id"], host_out["box"], host_out["objectness"],
+                                frames, B)
+        return OnlineTracks(eng.rec_count[:F], eng.rec_id[:F], eng.rec_box[:F], eng.rec_obj[:F], frames, B)
+
+    def host_output(self, frames: int) -> dict:
+        torch = self.engine.torch
+        R = self.engine.cap.max_detections
+        return dict(count=torch.zeros(frames, dtype=torch.int32).pin_memory(),
+                    track_id=torch.zeros(frames, R, dtype=torch.int64).pin_memory(),
+                    box=torch.zeros(frames, R, 4, dtype=torch.float64).pin_memory(),
+                    objectness=torch.zeros(frames, R, dtype=torch.float64).pin_memory())
+
+    def trace(self, frames: int) -> dict:
+        """Per-frame parity trace of the last traced update (device tensors)."""
+        e = self.engine
+        return dict(cand_count=e.tr_cand[:frames], det_count=e.tr_det[:frames], det_code=e.tr_code[:frames],
+                    det_track=e.tr_track[:frames], det_cost=e.tr_cost[:frames], det_matched=e.tr_matched[:frames])
+
+    def export(self, stream: int) -> dict:
+        return self.engine.export(stream)

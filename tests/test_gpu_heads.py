@@ -1,0 +1,160 @@
+"""GPU parity of the batched update(head_outputs) path against the CPU oracle.
+
+Inputs are generated on the device, copied back, and decoded + tracked by the
+oracle (oracle/heads.py + oracle/tracker.py). Bit-exact: kept detection
+indices (global anchor codes), association pairs (detection -> track id),
+record ids. Values: boxes, objectness, match costs within 1e-4 relative
+(the north-star tolerance; observed errors are reported and are ~1e-15).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import tracker as ot   # noqa: E402
+from parity import FrameCompare, host_frames, oracle_settings, run_oracle_frame   # noqa: E402
+
+
+def _pkg():
+    import paper_2011_03910_b200 as p
+    from paper_2011_03910_b200 import synth
+    return p, synth
+
+
+def _run_parity(cfg_name, steps, B, streams=1, quantize=False, literal=False, config=None, max_tracks=256,
+                **synth_kw):
+    p, synth = _pkg()
+    cfg = config or p.TrackerConfig()
+    gen = synth.make(cfg_name, device="cuda", streams=streams, literal_noise=literal, **synth_kw)
+    cap = p.Capacity(streams=streams, max_frames=streams * B, max_tracks=max_tracks)
+    bt = p.BatchTracker(streams, cfg, frames_per_update=B, quantize=quantize, capacity=cap)
+    oracles = [ot.OracleTracker(oracle_settings(cfg, quantize)) for _ in range(streams)]
+    cmp = FrameCompare()
+    frame = 0
+    for step in range(steps):
+        out = gen.next_batch(B)
+        fidx = np.array([[frame + b for b in range(B)] for _ in range(streams)], np.int64)
+        res = bt.update(out, fidx, trace=True)
+        tr = {k: v.cpu().numpy() for k, v in bt.trace(streams * B).items()}
+        cnt = res.count.cpu().numpy()
+        ids, boxes, objs = res.track_id.cpu().numpy(), res.box.cpu().numpy(), res.objectness.cpu().numpy()
+        host = host_frames(out, range(streams * B))
+        for s in range(streams):
+            for b in range(B):
+                f = s * B + b
+                codes, trace = run_oracle_frame(oracles[s], frame + b, *host[f], quantize=quantize)
+                assert tr["cand_count"][f] == len(codes), f"candidate count differs at frame {f}"
+                k = tr["det_count"][f]
+                recs = [(int(ids[f, i]), tuple(boxes[f, i]), float(objs[f, i])) for i in range(cnt[f])]
+                cmp.check(frame + b, trace, recs, tr["det_code"][f, :k], tr["det_track"][f, :k],
+                          tr["det_cost"][f, :k], tr["det_matched"][f, :k], codes)
+        frame += B
+    # final track tables
+    for s in range(streams):
+        ex = bt.export(s)
+        o = oracles[s]
+        assert ex["track_id"].tolist() == [t.track_id for t in o.tracks]
+        assert ex["hits"].tolist() == [t.hits for t in o.tracks]
+        assert [int(v) for v in ex["state"]] == [int(t.state == ot.LOST) for t in o.tracks]
+        for i, t in enumerate(o.tracks):
+            np.testing.assert_allclose(ex["mean"][i], t.mean, rtol=1e-4, atol=1e-6)
+            np.testing.assert_allclose(ex["covariance"][i], t.cov, rtol=1e-4, atol=1e-9)
+            np.testing.assert_allclose(ex["embedding"][i], t.emb, rtol=1e-4, atol=1e-6)
+        assert ex["next_id"] == o.next_id
+    return cmp
+
+
+def test_cfg0_single_stream_b1():
+    cmp = _run_parity("cfg0", steps=40, B=1)
+    assert cmp.matches > 500
+    print(f"cfg0: frames={cmp.frames} records={cmp.records} matches={cmp.matches} "
+          f"box_rel={cmp.max_box_rel:.2e} cost_rel={cmp.max_cost_rel:.2e}")
+
+
+def test_cfg1_batch32():
+    cmp = _run_parity("cfg1", steps=3, B=32)
+    print(f"cfg1/B32: frames={cmp.frames} records={cmp.records} matches={cmp.matches} "
+          f"box_rel={cmp.max_box_rel:.2e} cost_rel={cmp.max_cost_rel:.2e}")
+
+
+def test_multi_stream_cfg3_like():
+    cmp = _run_parity("cfg3", steps=3, B=8, streams=6)
+    assert cmp.frames == 6 * 24
+
+
+def test_dense_scene_cfg2_like():
+    cmp = _run_parity("cfg2", steps=2, B=8)
+    assert cmp.records > 1000
+
+
+def test_mixed_precision_quantize():
+    _run_parity("cfg0", steps=12, B=2, quantize=True)
+
+
+def test_literal_noise_stress():
+    _run_parity("cfg0", steps=10, B=2, literal=True, max_tracks=1024)
+
+
+def test_euclidean_and_lifecycle_knobs():
+    p, _ = _pkg()
+    cfg = p.TrackerConfig(gate_metric="euclidean", gate_threshold=2500.0, max_lost=3, min_hits=2)
+    _run_parity("cfg0", steps=10, B=3, config=cfg)
+
+
+def test_host_pinned_input_matches_device_input():
+    p, synth = _pkg()
+    gen = synth.make("cfg1", device="cuda")
+    out = gen.next_batch(8)
+    dev = p.BatchTracker(1, frames_per_update=8)
+    host = p.BatchTracker(1, frames_per_update=8)
+    r1 = dev.update(out)
+    pinned = p.HeadOutputs(tuple(h.cpu().pin_memory() for h in out.heads),
+                           tuple(e.cpu().pin_memory() for e in out.embs))
+    # keep channels_last on the host copy so the gather stays contiguous
+    pinned = p.HeadOutputs(pinned.heads, tuple(e.contiguous(memory_format=torch.channels_last).pin_memory()
+                                               for e in pinned.embs))
+    r2 = host.update(pinned)
+    assert np.array_equal(r1.count.cpu().numpy(), r2.count.numpy())
+    for f in range(8):
+        n = int(r2.count[f])
+        assert np.array_equal(r1.track_id[f, :n].cpu().numpy(), r2.track_id[f, :n].numpy())
+        assert np.array_equal(r1.box[f, :n].cpu().numpy(), r2.box[f, :n].numpy())
+
+
+def test_ordering_error_and_capacity():
+    p, synth = _pkg()
+    gen = synth.make("cfg0", device="cuda")
+    bt = p.BatchTracker(1, frames_per_update=2)
+    bt.update(gen.next_batch(2), np.array([5, 6]))
+    with pytest.raises(p.OrderingError):
+        bt.update(gen.next_batch(2), np.array([6, 7]))
+    small = p.BatchTracker(1, frames_per_update=1, capacity=p.Capacity(streams=1, max_frames=1,
+                                                                           max_candidates=8))
+    with pytest.raises(p.CapacityError):
+        small.update(gen.next_batch(1))
+
+
+def test_full_size_cfg4_step_properties():
+    """One cfg4-sized step (512 streams x 8 frames): size-independent invariants."""
+    p, synth = _pkg()
+    gen = synth.make("cfg4", device="cuda", streams=512)
+    bt = p.BatchTracker(512, frames_per_update=8)
+    last_max = np.zeros(512, np.int64)
+    for _ in range(2):
+        res = bt.update(gen.next_batch(8), trace=True)
+        cnt = res.count.cpu().numpy()
+        ids = res.track_id.cpu().numpy()
+        tr = bt.trace(512 * 8)
+        det = tr["det_count"].cpu().numpy()
+        assert np.array_equal(cnt, det)              # min_hits = 1: every kept detection is reported
+        for f in range(512 * 8):
+            row = ids[f, :cnt[f]]
+            assert np.all(np.diff(row) > 0)          # sorted by id, unique
+        for s in range(512):
+            blk = ids[s * 8:(s + 1) * 8]
+            m = blk.max() if blk.size else 0
+            assert m >= last_max[s]
+            last_max[s] = m
