@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(512) frame_dets_kernel(RowsArgs a, Params P) {
 // ============================================================================
 
 struct AssocPlan {
-  size_t off_id, off_lost, off_last, off_mean, off_cov, off_pm, off_il, off_mcost, off_state, off_hits,
+  size_t off_id, off_lost, off_last, off_mean, off_cov, off_il, off_mcost, off_state, off_hits,
       off_slot, off_mdet, off_rowptr, off_flag, off_npos, off_rpos, off_dm, off_dobj, off_drow, off_dpos, off_gmask,
       off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
       off_vr, off_vc, total;
@@ -420,7 +420,6 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_last, 8 * T)
   TF_TAKE(off_mean, 8 * 8 * T)
   TF_TAKE(off_cov, 8 * 12 * T)
-  TF_TAKE(off_pm, 8 * 4 * T)
   TF_TAKE(off_il, 8 * 4 * T)
   TF_TAKE(off_mcost, 8 * T)
   TF_TAKE(off_state, 4 * T)
@@ -467,7 +466,6 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
   int64_t* t_last = reinterpret_cast<int64_t*>(smem + pl.off_last);
   double* t_mean = reinterpret_cast<double*>(smem + pl.off_mean);
   double* t_cov = reinterpret_cast<double*>(smem + pl.off_cov);
-  double* t_pm = reinterpret_cast<double*>(smem + pl.off_pm);
   double* t_il = reinterpret_cast<double*>(smem + pl.off_il);
   double* t_mcost = reinterpret_cast<double*>(smem + pl.off_mcost);
   int* t_state = reinterpret_cast<int*>(smem + pl.off_state);

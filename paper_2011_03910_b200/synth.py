@@ -147,8 +147,8 @@ class HeadSynth:
         for s in STRIDES:
             H, W = GRID[s]
             heads.append(torch.empty(frames, 24, H, W, dtype=torch.float32, device=self.device))
-            embs.append(torch.empty(frames, self.cfg.dim, H, W, dtype=torch.float32, device=self.device)
-                        .contiguous(memory_format=torch.channels_last))
+            embs.append(torch.empty(frames, self.cfg.dim, H, W, dtype=torch.float32, device=self.device,
+                                    memory_format=torch.channels_last))
         return HeadOutputs(tuple(heads), tuple(embs))
 
     def _background(self, out: HeadOutputs):

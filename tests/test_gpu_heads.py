@@ -95,7 +95,7 @@ def test_mixed_precision_quantize():
 
 
 def test_literal_noise_stress():
-    _run_parity("cfg0", steps=10, B=2, literal=True, max_tracks=1024)
+    _run_parity("cfg0", steps=10, B=2, literal=True, max_tracks=512)
 
 
 def test_euclidean_and_lifecycle_knobs():
