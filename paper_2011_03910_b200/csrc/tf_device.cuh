@@ -308,15 +308,41 @@ __device__ int block_rank(int n, FlagFn flag, int16_t* pos, int* sh_warp /* [33]
 // list position for free columns, the earlier one otherwise), so the returned
 // optimum is the one the reference gets, ties included.
 //
-// Row r < nr has its finite entries as CSR (rowptr, ecol, eval); every other
+// Row r < nr has its finite entries given by a row accessor `R` (global CSR or
+// a connected component's submatrix, see CsrRows / ComponentRows); every other
 // cell (including rows >= nr and columns >= nc) costs `sentinel`.
 struct LapScratch {
   double *u, *v, *dist, *crow;
   int16_t *path, *row4col, *col4row, *rem, *vrows, *vcols;
 };
 
-__device__ inline void warp_lap(int n, int nr, const int* rowptr, const int16_t* ecol, const double* eval,
-                         double sentinel, LapScratch s) {
+// Finite entries of row r of the full gated matrix (CSR by row).
+struct CsrRows {
+  const int* rowptr;
+  const int16_t* ecol;
+  const double* eval;
+  __device__ __forceinline__ int begin(int r) const { return rowptr[r]; }
+  __device__ __forceinline__ int end(int r) const { return rowptr[r + 1]; }
+  __device__ __forceinline__ int col(int e) const { return ecol[e]; }
+  __device__ __forceinline__ double val(int e) const { return eval[e]; }
+};
+
+// Finite entries of local row r of one connected component: local rows map to
+// global rows (ascending), global columns map to local columns.
+struct ComponentRows {
+  const int* rowptr;
+  const int16_t* ecol;
+  const double* eval;
+  const int16_t* rows;     // local row -> global row
+  const int16_t* colmap;   // global column -> local column
+  __device__ __forceinline__ int begin(int r) const { return rowptr[rows[r]]; }
+  __device__ __forceinline__ int end(int r) const { return rowptr[rows[r] + 1]; }
+  __device__ __forceinline__ int col(int e) const { return colmap[ecol[e]]; }
+  __device__ __forceinline__ double val(int e) const { return eval[e]; }
+};
+
+template <class Rows>
+__device__ inline void warp_lap(int n, int nr, const Rows R, double sentinel, LapScratch s) {
   const int lane = lane_id();
   for (int j = lane; j < n; j += 32) {
     s.u[j] = 0.0;
@@ -337,9 +363,9 @@ __device__ inline void warp_lap(int n, int nr, const int* rowptr, const int16_t*
       ++nvr;
       int e0 = 0, e1 = 0;
       if (row < nr) {
-        e0 = rowptr[row];
-        e1 = rowptr[row + 1];
-        for (int e = e0 + lane; e < e1; e += 32) s.crow[ecol[e]] = eval[e];
+        e0 = R.begin(row);
+        e1 = R.end(row);
+        for (int e = e0 + lane; e < e1; e += 32) s.crow[R.col(e)] = R.val(e);
       }
       __syncwarp();
       const double ur = s.u[row];
@@ -367,7 +393,7 @@ __device__ inline void warp_lap(int n, int nr, const int* rowptr, const int16_t*
       }
       __syncwarp();
       if (row < nr)
-        for (int e = e0 + lane; e < e1; e += 32) s.crow[ecol[e]] = sentinel;
+        for (int e = e0 + lane; e < e1; e += 32) s.crow[R.col(e)] = sentinel;
       // warp argmin with the tie rule
       const unsigned hi = static_cast<unsigned>(best >> 32), lo = static_cast<unsigned>(best);
       const unsigned mh = __reduce_min_sync(FULL, hi);

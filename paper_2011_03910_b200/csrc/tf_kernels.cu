@@ -84,17 +84,17 @@ __device__ int gather_normalize(const float* src, long long stride, int dim, int
       float4 q = __ldg(s4 + i);
       double a = q.x, b = q.y, c = q.z, d = q.w;
       finite = finite && isfinite(q.x) && isfinite(q.y) && isfinite(q.z) && isfinite(q.w);
-      ss += a * a;
-      ss += b * b;
-      ss += c * c;
-      ss += d * d;
+      ss = fma(a, a, ss);
+      ss = fma(b, b, ss);
+      ss = fma(c, c, ss);
+      ss = fma(d, d, ss);
     }
   } else {
     for (int i = lane; i < dim; i += 32) {
       float x = __ldg(src + static_cast<long long>(i) * stride);
       finite = finite && isfinite(x);
       double a = x;
-      ss += a * a;
+      ss = fma(a, a, ss);
     }
   }
   ss = warp_sum(ss);
@@ -406,12 +406,13 @@ struct AssocPlan {
   size_t off_id, off_lost, off_last, off_mean, off_cov, off_il, off_mcost, off_state, off_hits,
       off_slot, off_mdet, off_rowptr, off_flag, off_npos, off_rpos, off_dm, off_dobj, off_drow, off_dpos, off_gmask,
       off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
-      off_vr, off_vc, total;
+      off_vr, off_vc, off_lab, off_cnr, off_cnc, off_cne, off_croot, off_coff, off_cpos, off_crows, off_ccols,
+      off_cmap, off_rcol, total;
 };
 
 __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   AssocPlan p;
-  const int N = T > K ? T : K;
+  const int NN = T + K;
   const int KW = (K + 31) / 32;
   size_t o = 0;
 #define TF_TAKE(field, bytes) p.field = o; o = align16(o + (bytes));
@@ -438,16 +439,29 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_ecol, 2 * E)
   TF_TAKE(off_erow, 2 * E)
   TF_TAKE(off_eval, 8 * E)
-  TF_TAKE(off_u, 8 * N)
-  TF_TAKE(off_v, 8 * N)
-  TF_TAKE(off_dist, 8 * N)
-  TF_TAKE(off_crow, 8 * N)
-  TF_TAKE(off_path, 2 * N)
-  TF_TAKE(off_r4c, 2 * N)
-  TF_TAKE(off_c4r, 2 * N)
-  TF_TAKE(off_rem, 2 * N)
-  TF_TAKE(off_vr, 2 * (N + 1))
-  TF_TAKE(off_vc, 2 * (N + 1))
+  // LAP scratch: N for the full solve, or disjoint per-component slices (sum <= T + K)
+  TF_TAKE(off_u, 8 * NN)
+  TF_TAKE(off_v, 8 * NN)
+  TF_TAKE(off_dist, 8 * NN)
+  TF_TAKE(off_crow, 8 * NN)
+  TF_TAKE(off_path, 2 * NN)
+  TF_TAKE(off_r4c, 2 * NN)
+  TF_TAKE(off_c4r, 2 * NN)
+  TF_TAKE(off_rem, 2 * NN)
+  TF_TAKE(off_vr, 2 * (2 * NN + 1))
+  TF_TAKE(off_vc, 2 * (2 * NN + 1))
+  // connected components
+  TF_TAKE(off_lab, 4 * NN)
+  TF_TAKE(off_cnr, 4 * NN)
+  TF_TAKE(off_cnc, 4 * NN)
+  TF_TAKE(off_cne, 4 * NN)
+  TF_TAKE(off_croot, 4 * NN)
+  TF_TAKE(off_coff, 4 * (NN + 1))
+  TF_TAKE(off_cpos, 2 * NN)
+  TF_TAKE(off_crows, 2 * NN)
+  TF_TAKE(off_ccols, 2 * NN)
+  TF_TAKE(off_cmap, 2 * K)
+  TF_TAKE(off_rcol, 2 * T)
 #undef TF_TAKE
   p.total = o;
   return p;
@@ -492,9 +506,20 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
   L.rem = reinterpret_cast<int16_t*>(smem + pl.off_rem);
   L.vrows = reinterpret_cast<int16_t*>(smem + pl.off_vr);
   L.vcols = reinterpret_cast<int16_t*>(smem + pl.off_vc);
+  int* c_lab = reinterpret_cast<int*>(smem + pl.off_lab);
+  int* c_nr = reinterpret_cast<int*>(smem + pl.off_cnr);
+  int* c_nc = reinterpret_cast<int*>(smem + pl.off_cnc);
+  int* c_ne = reinterpret_cast<int*>(smem + pl.off_cne);
+  int* c_root = reinterpret_cast<int*>(smem + pl.off_croot);
+  int* c_off = reinterpret_cast<int*>(smem + pl.off_coff);
+  int16_t* c_pos = reinterpret_cast<int16_t*>(smem + pl.off_cpos);
+  int16_t* c_rows = reinterpret_cast<int16_t*>(smem + pl.off_crows);
+  int16_t* c_cols = reinterpret_cast<int16_t*>(smem + pl.off_ccols);
+  int16_t* c_map = reinterpret_cast<int16_t*>(smem + pl.off_cmap);
+  int16_t* rcol = reinterpret_cast<int16_t*>(smem + pl.off_rcol);
 
   __shared__ int s_warp[33];
-  __shared__ int s_T, s_status, s_E, s_nfree, s_err;
+  __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie;
   __shared__ long long s_next;
   __shared__ double s_amp;
 
@@ -623,29 +648,50 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
       }
       __syncthreads();
       // ---- fp64 cosine cost of un-gated pairs (tf/assoc.py:34-46) ----------
+      // fp32 x fp32 products are exact in fp64, so fma == mul + add bit for bit.
+      // Two entries per warp iteration keep 16 x 128-bit loads in flight per lane.
       double amp = 0.0;
-      for (int e = wid; e < E; e += nw) {
-        const int t = erow[e], k = ecol[e];
-        const float* te = a.trk.emb_pool + (sT + t_slot[t]) * static_cast<long long>(D);
-        const float* de = a.det.emb + (fK + k) * static_cast<long long>(D);
-        double acc = 0.0;
+      for (int e0 = 2 * wid; e0 < E; e0 += 2 * nw) {
+        const bool two = e0 + 1 < E;
+        const int e1 = two ? e0 + 1 : e0;
+        const float* te0 = a.trk.emb_pool + (sT + t_slot[erow[e0]]) * static_cast<long long>(D);
+        const float* de0 = a.det.emb + (fK + ecol[e0]) * static_cast<long long>(D);
+        const float* te1 = a.trk.emb_pool + (sT + t_slot[erow[e1]]) * static_cast<long long>(D);
+        const float* de1 = a.det.emb + (fK + ecol[e1]) * static_cast<long long>(D);
+        double acc0 = 0.0, acc1 = 0.0;
         if ((D & 3) == 0) {
-          const float4* t4 = reinterpret_cast<const float4*>(te);
-          const float4* d4 = reinterpret_cast<const float4*>(de);
+          const float4 *t40 = reinterpret_cast<const float4*>(te0), *d40 = reinterpret_cast<const float4*>(de0);
+          const float4 *t41 = reinterpret_cast<const float4*>(te1), *d41 = reinterpret_cast<const float4*>(de1);
           for (int i = lane; i < D / 4; i += 32) {
-            float4 x = t4[i], y = d4[i];
-            acc += static_cast<double>(x.x) * static_cast<double>(y.x);
-            acc += static_cast<double>(x.y) * static_cast<double>(y.y);
-            acc += static_cast<double>(x.z) * static_cast<double>(y.z);
-            acc += static_cast<double>(x.w) * static_cast<double>(y.w);
+            const float4 x0 = t40[i], y0 = d40[i], x1 = t41[i], y1 = d41[i];
+            acc0 = fma(static_cast<double>(x0.x), static_cast<double>(y0.x), acc0);
+            acc1 = fma(static_cast<double>(x1.x), static_cast<double>(y1.x), acc1);
+            acc0 = fma(static_cast<double>(x0.y), static_cast<double>(y0.y), acc0);
+            acc1 = fma(static_cast<double>(x1.y), static_cast<double>(y1.y), acc1);
+            acc0 = fma(static_cast<double>(x0.z), static_cast<double>(y0.z), acc0);
+            acc1 = fma(static_cast<double>(x1.z), static_cast<double>(y1.z), acc1);
+            acc0 = fma(static_cast<double>(x0.w), static_cast<double>(y0.w), acc0);
+            acc1 = fma(static_cast<double>(x1.w), static_cast<double>(y1.w), acc1);
           }
         } else {
-          for (int i = lane; i < D; i += 32) acc += static_cast<double>(te[i]) * static_cast<double>(de[i]);
+          for (int i = lane; i < D; i += 32) {
+            acc0 = fma(static_cast<double>(te0[i]), static_cast<double>(de0[i]), acc0);
+            acc1 = fma(static_cast<double>(te1[i]), static_cast<double>(de1[i]), acc1);
+          }
         }
-        acc = warp_sum(acc);
-        double cval = fmin(fmax(1.0 - acc, 0.0), 2.0);
-        if (lane == 0) eval[e] = cval;
-        amp = fmax(amp, fabs(cval));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc0 += __shfl_xor_sync(FULL, acc0, o);
+          acc1 += __shfl_xor_sync(FULL, acc1, o);
+        }
+        const double c0 = fmin(fmax(1.0 - acc0, 0.0), 2.0);
+        const double c1 = fmin(fmax(1.0 - acc1, 0.0), 2.0);
+        if (lane == 0) {
+          eval[e0] = c0;
+          if (two) eval[e1] = c1;
+        }
+        amp = fmax(amp, fabs(c0));
+        if (two) amp = fmax(amp, fabs(c1));
       }
       if (lane == 0 && E > 0) {
         // amplitude = max |finite| (tf/assoc.py:71); non-negative, so an
@@ -659,34 +705,142 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
       break;
     }
 
-    // ---- exact LAP on the sentinel-padded matrix (tf/assoc.py:60-87) -------
-    if (gating && wid == 0) {
-      const int n = T > K ? T : K;
-      const double sentinel = 2.0 * static_cast<double>(n) * fmax(s_amp, 1.0) + 1.0;
-      warp_lap(n, T, rowptr, ecol, eval, sentinel, L);
-    }
-    __syncthreads();
-    // ---- matches + max_cost threshold (tf/assoc.py:77-107) -----------------
+    // ---- exact LAP (tf/assoc.py:60-87), decomposed by connected components --
+    // The padded problem (sentinel everywhere but the finite entries) maximises
+    // the number of finite pairs, then minimises their cost; it separates over
+    // the connected components of the finite bipartite graph whenever the
+    // optimum is unique. Single-edge components are matched directly, larger
+    // components are solved by one warp each with the same exact solver on the
+    // component's submatrix. When a component holds two equal costs (a genuine
+    // tie: e.g. two detections sharing one cell's embedding) the whole padded
+    // matrix is solved by the scipy-order restatement instead, so the tie is
+    // broken exactly as the reference breaks it.
     if (gating) {
-      for (int t = tid; t < T; t += blockDim.x) {
-        const int c = L.col4row[t];
-        int md = -1;
-        double mc = 0.0;
-        if (c < K) {
-          for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
-            if (ecol[e] == c) {
-              mc = eval[e];
-              md = (mc > P.max_cost) ? -1 : c;
-              break;
-            }
+      const int E = s_E;
+      const int NN = T + K;
+      for (int x = tid; x < NN; x += blockDim.x) {
+        c_lab[x] = x;
+        c_nr[x] = 0;
+        c_nc[x] = 0;
+        c_ne[x] = 0;
+      }
+      for (int t = tid; t < T; t += blockDim.x) rcol[t] = -1;
+      if (tid == 0) { s_flag = 1; s_tie = (E > 1024); }
+      for (;;) {
+        __syncthreads();
+        const int go = s_flag;
+        __syncthreads();
+        if (!go) break;
+        if (tid == 0) s_flag = 0;
+        __syncthreads();
+        for (int e = tid; e < E; e += blockDim.x) {
+          const int r = erow[e], c = T + ecol[e];
+          const int la = c_lab[r], lb = c_lab[c];
+          if (la != lb) {
+            const int m = min(la, lb);
+            atomicMin(&c_lab[r], m);
+            atomicMin(&c_lab[c], m);
+            s_flag = 1;
+          }
         }
-        t_mdet[t] = md;
-        t_mcost[t] = mc;
-        if (md >= 0) d_row[md] = t;
+        __syncthreads();
+        for (int x = tid; x < NN; x += blockDim.x) {       // pointer jumping (monotone)
+          const int l = c_lab[x], ll = c_lab[l];
+          if (ll < l) c_lab[x] = ll;
+        }
+      }
+      for (int x = tid; x < NN; x += blockDim.x) atomicAdd(x < T ? &c_nr[c_lab[x]] : &c_nc[c_lab[x]], 1);
+      for (int e = tid; e < E; e += blockDim.x) {
+        const int root = c_lab[erow[e]];
+        atomicAdd(&c_ne[root], 1);
+        if (!s_tie) {
+          const double v0 = eval[e];
+          for (int e2 = e + 1; e2 < E; ++e2)
+            if (eval[e2] == v0 && c_lab[erow[e2]] == root) { s_tie = 1; break; }
+        }
+      }
+      __syncthreads();
+      if (s_tie) {
+        if (wid == 0) {
+          const int n = T > K ? T : K;
+          const double sentinel = 2.0 * static_cast<double>(n) * fmax(s_amp, 1.0) + 1.0;
+          warp_lap(n, T, CsrRows{rowptr, ecol, eval}, sentinel, L);
+          __syncwarp();
+          for (int t = lane; t < T; t += 32) {
+            const int c = L.col4row[t];
+            rcol[t] = static_cast<int16_t>(c < K ? c : -1);
+          }
+        }
+      } else {
+        // single-edge components
+        for (int e = tid; e < E; e += blockDim.x) {
+          const int root = c_lab[erow[e]];
+          if (c_nr[root] == 1 && c_nc[root] == 1) rcol[erow[e]] = ecol[e];
+        }
+        // multi-edge components: ordered list, scratch slices, one warp each
+        const int n_multi = block_rank(NN, [&](int x) { return c_lab[x] == x && c_ne[x] >= 2; }, c_pos, s_warp);
+        for (int x = tid; x < NN; x += blockDim.x)
+          if (c_pos[x] >= 0) c_root[c_pos[x]] = x;
+        __syncthreads();
+        if (wid == 0) {
+          int carry = 0;
+          for (int i0 = 0; i0 < n_multi; i0 += 32) {
+            const int i = i0 + lane;
+            int v = 0;
+            if (i < n_multi) v = max(c_nr[c_root[i]], c_nc[c_root[i]]);
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              int q = __shfl_up_sync(FULL, incl, o);
+              if (lane >= o) incl += q;
+            }
+            if (i < n_multi) c_off[i] = carry + incl - v;
+            carry += __shfl_sync(FULL, incl, 31);
+          }
+        }
+        __syncthreads();
+        for (int i = wid; i < n_multi; i += nw) {
+          const int root = c_root[i], off = c_off[i];
+          int nr_l = 0, nc_l = 0;
+          for (int t0 = 0; t0 < T; t0 += 32) {
+            const int t = t0 + lane;
+            const bool in = t < T && c_lab[t] == root;
+            const unsigned bm = __ballot_sync(FULL, in);
+            if (in) c_rows[off + nr_l + __popc(bm & ((1u << lane) - 1u))] = static_cast<int16_t>(t);
+            nr_l += __popc(bm);
+          }
+          for (int k0 = 0; k0 < K; k0 += 32) {
+            const int k = k0 + lane;
+            const bool in = k < K && c_lab[T + k] == root;
+            const unsigned bm = __ballot_sync(FULL, in);
+            if (in) {
+              const int j = nc_l + __popc(bm & ((1u << lane) - 1u));
+              c_cols[off + j] = static_cast<int16_t>(k);
+              c_map[k] = static_cast<int16_t>(j);
+            }
+            nc_l += __popc(bm);
+          }
+          __syncwarp();
+          const int n_l = nr_l > nc_l ? nr_l : nc_l;
+          LapScratch Ls;
+          Ls.u = L.u + off; Ls.v = L.v + off; Ls.dist = L.dist + off; Ls.crow = L.crow + off;
+          Ls.path = L.path + off; Ls.row4col = L.row4col + off; Ls.col4row = L.col4row + off;
+          Ls.rem = L.rem + off; Ls.vrows = L.vrows + off + i; Ls.vcols = L.vcols + off + i;
+          const double sentinel = 2.0 * static_cast<double>(n_l) * fmax(s_amp, 1.0) + 1.0;
+          warp_lap(n_l, nr_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, Ls);
+          __syncwarp();
+          for (int r = lane; r < nr_l; r += 32) {
+            const int j = Ls.col4row[r];
+            if (j < nc_l) {
+              const int t = c_rows[off + r], c = c_cols[off + j];
+              for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
+                if (ecol[e] == c) { rcol[t] = static_cast<int16_t>(c); break; }
+            }
+          }
+        }
       }
     }
     __syncthreads();
-
     // ---- matched: Kalman update + lifecycle (tf/tracker.py:114-125) --------
     for (int t = tid; t < T; t += blockDim.x) {
       const int k = t_mdet[t];
@@ -970,7 +1124,7 @@ __global__ void lap_dense_kernel(const int* shapes, const long long* cost_off, c
   L.rem = reinterpret_cast<int16_t*>(smem + o); o += 2 * n;
   L.vrows = reinterpret_cast<int16_t*>(smem + o); o += 2 * (n + 1);
   L.vcols = reinterpret_cast<int16_t*>(smem + o);
-  warp_lap(n, nr, rowptr, ecol, eval, sentinel, L);
+  warp_lap(n, nr, CsrRows{rowptr, ecol, eval}, sentinel, L);
   __syncwarp();
   for (int r = lane; r < nr; r += 32) {
     int col = L.col4row[r];
