@@ -258,6 +258,9 @@ def run_ours(args):
     import ctypes as C
     fr_ms, as_ms, nup = C.c_double(), C.c_double(), C.c_int64()
     lib.tf_kernel_times(eng.ctx, C.byref(fr_ms), C.byref(as_ms), C.byref(nup))
+    import numpy as _np
+    phase = _np.zeros(32, _np.int64)
+    lib.tf_phase_stats(eng.ctx, phase.ctypes.data)
     lib.tf_set_profiling(eng.ctx, 0)
 
     # ---- end to end through the C ABI with pinned host buffers --------------
@@ -342,6 +345,16 @@ def run_ours(args):
                 "associate_kernel": {"ms_per_launch": assoc_launch_ms, "share_of_step":
                                      as_ms.value / max(ms, 1e-9)}},
             "per_frame": {"candidates": cand / (K * F), "detections": kpf, "records": rpf},
+            "assoc_phases_us_per_frame": {
+                name: float(phase[i]) / max(phase[11], 1) / (clocks.summary()["sm_mhz"] or 1965)
+                for i, name in list(enumerate(["load_predict", "gate", "csr", "cost", "lap", "match", "update_ema",
+                                               "records_births"]))
+                + [(16, "lap.components_tiecheck"), (17, "lap.peeling"), (18, "lap.residual_setup"),
+                   (19, "lap.warp_solves"), (20, "lap.full_restatement")]},
+            "assoc_counters_per_frame": {name: float(phase[i]) / max(phase[11], 1) for i, name in
+                                         [(8, "tie_fallback"), (9, "finite_entries"), (10, "multi_components"),
+                                          (14, "residual_entries"),
+                                          (12, "tracks"), (13, "detections")]},
             "gpu_launches": 2 * K,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,

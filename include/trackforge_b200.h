@@ -192,6 +192,14 @@ int tf_export_tracks(tf_ctx* ctx, int32_t stream, tf_track_export* out, void* cu
  * call, and resets the accumulators. */
 int tf_set_profiling(tf_ctx* ctx, int32_t enabled);
 int tf_kernel_times(tf_ctx* ctx, double* frame_ms, double* assoc_ms, int64_t* updates);
+/* Per-phase SM cycles of associate_kernel summed over streams since profiling
+ * was enabled (synchronising; resets): [0] load+predict [1] gate [2] CSR
+ * [3] cosine cost [4] LAP [5] matches [6] Kalman update + EMA [7] records,
+ * compaction, births; counters [8] tie fallbacks [9] finite entries
+ * [10] multi-edge components [11] frames [12] sum T [13] sum K; LAP sub-phases
+ * [16] components + tie check [17] peeling [18] residual components
+ * [19] warp solves [20] full restatement (ties). out has 32 entries. */
+int tf_phase_stats(tf_ctx* ctx, int64_t* out32);
 
 /* ---- stage-level entry points (batched; device pointers) ---------------- */
 

@@ -78,6 +78,7 @@ _SIGS = {
     "tf_export_tracks": (c_i32, [c_vp, c_i32, C.POINTER(TfTrackExport), c_vp]),
     "tf_set_profiling": (c_i32, [c_vp, c_i32]),
     "tf_kernel_times": (c_i32, [c_vp, C.POINTER(c_dbl), C.POINTER(c_dbl), C.POINTER(c_i64)]),
+    "tf_phase_stats": (c_i32, [c_vp, c_vp]),
     "tf_nms_sets": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tf_lap_dense": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tf_kalman": (c_i32, [c_i32, c_i32, C.POINTER(TfConfig), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -51,6 +51,7 @@ struct tf_ctx {
   std::vector<cudaEvent_t> events;   // triples: before frame kernel, after it, after associate
   size_t events_used;
   long long prof_bytes_frame, prof_frames;
+  long long* d_stats;
   std::vector<void*> allocs;
 };
 
@@ -282,6 +283,7 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   A(&c->pool_col, S * Tm * Km);
   A(&c->pool_row, S * Tm * Km);
   A(&c->pool_val, S * Tm * Km);
+  A(&c->d_stats, 32);
   if (e != cudaSuccess) {
     std::string m = cudaGetErrorString(e);
     tf_destroy(c);
@@ -439,6 +441,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
+  a.stats = c->profiling ? c->d_stats : nullptr;
   const bool host_out = heads->host_memory != 0;
   if (host_out) {
     rc = ensure_record_staging(c, F, out->max_records);
@@ -504,6 +507,7 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
+  a.stats = c->profiling ? c->d_stats : nullptr;
   a.out.count = out->count;
   a.out.track_id = reinterpret_cast<long long*>(out->track_id);
   a.out.box = out->box;
@@ -581,6 +585,15 @@ int tf_set_profiling(tf_ctx* c, int32_t enabled) {
   if (!c) return TF_ARGUMENT;
   c->profiling = enabled;
   c->events_used = 0;
+  TF_CUDA(c, cudaMemset(c->d_stats, 0, 32 * sizeof(long long)));
+  return TF_OK;
+}
+
+int tf_phase_stats(tf_ctx* c, int64_t* out16) {
+  if (!c || !out16) return TF_ARGUMENT;
+  TF_CUDA(c, cudaDeviceSynchronize());
+  TF_CUDA(c, cudaMemcpy(out16, c->d_stats, 32 * sizeof(long long), cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemset(c->d_stats, 0, 32 * sizeof(long long)));
   return TF_OK;
 }
 

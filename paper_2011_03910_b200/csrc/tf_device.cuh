@@ -365,7 +365,10 @@ __device__ inline void warp_lap(int n, int nr, const Rows R, double sentinel, La
       if (row < nr) {
         e0 = R.begin(row);
         e1 = R.end(row);
-        for (int e = e0 + lane; e < e1; e += 32) s.crow[R.col(e)] = R.val(e);
+        for (int e = e0 + lane; e < e1; e += 32) {
+          const int c = R.col(e);
+          if (c >= 0) s.crow[c] = R.val(e);
+        }
       }
       __syncwarp();
       const double ur = s.u[row];
@@ -393,7 +396,10 @@ __device__ inline void warp_lap(int n, int nr, const Rows R, double sentinel, La
       }
       __syncwarp();
       if (row < nr)
-        for (int e = e0 + lane; e < e1; e += 32) s.crow[R.col(e)] = sentinel;
+        for (int e = e0 + lane; e < e1; e += 32) {
+          const int c = R.col(e);
+          if (c >= 0) s.crow[c] = sentinel;
+        }
       // warp argmin with the tie rule
       const unsigned hi = static_cast<unsigned>(best >> 32), lo = static_cast<unsigned>(best);
       const unsigned mh = __reduce_min_sync(FULL, hi);

@@ -403,11 +403,12 @@ __global__ void __launch_bounds__(512) frame_dets_kernel(RowsArgs a, Params P) {
 // ============================================================================
 
 struct AssocPlan {
-  size_t off_id, off_lost, off_last, off_mean, off_cov, off_il, off_mcost, off_state, off_hits,
+  size_t off_id, off_lost, off_last, off_mean, off_cov, off_mcost, off_state, off_hits,
       off_slot, off_mdet, off_rowptr, off_flag, off_npos, off_rpos, off_dm, off_dobj, off_drow, off_dpos, off_gmask,
       off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
       off_vr, off_vc, off_lab, off_cnr, off_cnc, off_cne, off_croot, off_coff, off_cpos, off_crows, off_ccols,
-      off_cmap, off_rcol, total;
+      off_cmap, off_rcol, off_epos, off_elist, off_pcmin, off_prmin, off_pccnt, off_pcdeg, off_pcrow, off_prdeg, off_prcnt, off_prc1,
+      off_pra, off_pca, off_pkr, off_pkc, total;
 };
 
 __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
@@ -421,7 +422,6 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_last, 8 * T)
   TF_TAKE(off_mean, 8 * 8 * T)
   TF_TAKE(off_cov, 8 * 12 * T)
-  TF_TAKE(off_il, 8 * 4 * T)
   TF_TAKE(off_mcost, 8 * T)
   TF_TAKE(off_state, 4 * T)
   TF_TAKE(off_hits, 4 * T)
@@ -435,7 +435,6 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_dobj, 8 * K)
   TF_TAKE(off_drow, 4 * K)
   TF_TAKE(off_dpos, 2 * K)
-  TF_TAKE(off_gmask, 4 * T * KW)
   TF_TAKE(off_ecol, 2 * E)
   TF_TAKE(off_erow, 2 * E)
   TF_TAKE(off_eval, 8 * E)
@@ -450,7 +449,10 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_rem, 2 * NN)
   TF_TAKE(off_vr, 2 * (2 * NN + 1))
   TF_TAKE(off_vc, 2 * (2 * NN + 1))
-  // connected components
+  // connected components / peeling; the gate bitmask (dead once the CSR is
+  // built) shares this region
+  const size_t ustart = o;
+  p.off_gmask = ustart;
   TF_TAKE(off_lab, 4 * NN)
   TF_TAKE(off_cnr, 4 * NN)
   TF_TAKE(off_cnc, 4 * NN)
@@ -462,12 +464,28 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_ccols, 2 * NN)
   TF_TAKE(off_cmap, 2 * K)
   TF_TAKE(off_rcol, 2 * T)
+  TF_TAKE(off_epos, 2 * E)
+  TF_TAKE(off_elist, 2 * E)
+  // forced-pair peeling
+  TF_TAKE(off_pcmin, 8 * K)
+  TF_TAKE(off_prmin, 8 * T)
+  TF_TAKE(off_pccnt, 4 * K)
+  TF_TAKE(off_pcdeg, 4 * K)
+  TF_TAKE(off_pcrow, 4 * K)
+  TF_TAKE(off_prdeg, 4 * T)
+  TF_TAKE(off_prcnt, 4 * T)
+  TF_TAKE(off_prc1, 4 * T)
+  TF_TAKE(off_pra, T)
+  TF_TAKE(off_pca, K)
+  TF_TAKE(off_pkr, T)
+  TF_TAKE(off_pkc, K)
+  if (o < align16(ustart + 4 * T * KW)) o = align16(ustart + 4 * T * KW);
 #undef TF_TAKE
   p.total = o;
   return p;
 }
 
-__global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, Params P) {
+__global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int ls = blockIdx.x;                 // local stream in this update
   const int s = a.stream_begin + ls;         // global stream id
@@ -480,7 +498,6 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
   int64_t* t_last = reinterpret_cast<int64_t*>(smem + pl.off_last);
   double* t_mean = reinterpret_cast<double*>(smem + pl.off_mean);
   double* t_cov = reinterpret_cast<double*>(smem + pl.off_cov);
-  double* t_il = reinterpret_cast<double*>(smem + pl.off_il);
   double* t_mcost = reinterpret_cast<double*>(smem + pl.off_mcost);
   int* t_state = reinterpret_cast<int*>(smem + pl.off_state);
   int* t_hits = reinterpret_cast<int*>(smem + pl.off_hits);
@@ -517,9 +534,44 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
   int16_t* c_cols = reinterpret_cast<int16_t*>(smem + pl.off_ccols);
   int16_t* c_map = reinterpret_cast<int16_t*>(smem + pl.off_cmap);
   int16_t* rcol = reinterpret_cast<int16_t*>(smem + pl.off_rcol);
+  int16_t* c_epos = reinterpret_cast<int16_t*>(smem + pl.off_epos);
+  int16_t* c_elist = reinterpret_cast<int16_t*>(smem + pl.off_elist);
+  unsigned long long* p_cmin = reinterpret_cast<unsigned long long*>(smem + pl.off_pcmin);
+  double* p_rmin = reinterpret_cast<double*>(smem + pl.off_prmin);
+  int* p_ccnt = reinterpret_cast<int*>(smem + pl.off_pccnt);
+  int* p_cdeg = reinterpret_cast<int*>(smem + pl.off_pcdeg);
+  int* p_crow = reinterpret_cast<int*>(smem + pl.off_pcrow);
+  int* p_rdeg = reinterpret_cast<int*>(smem + pl.off_prdeg);
+  int* p_rcnt = reinterpret_cast<int*>(smem + pl.off_prcnt);
+  int* p_rc1 = reinterpret_cast<int*>(smem + pl.off_prc1);
+  uint8_t* p_ra = smem + pl.off_pra;
+  uint8_t* p_ca = smem + pl.off_pca;
+  uint8_t* p_kr = smem + pl.off_pkr;
+  uint8_t* p_kc = smem + pl.off_pkc;
+  for (int x = threadIdx.x; x < Tm; x += blockDim.x) p_kr[x] = 0;
+  for (int x = threadIdx.x; x < Km; x += blockDim.x) p_kc[x] = 0;
 
   __shared__ int s_warp[33];
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie;
+  // optional phase timing (tf_set_profiling): cycles per phase + counters
+  __shared__ long long s_ph[32];
+  long long t_mark = 0, t_sub = 0;
+#define TF_SUB(i)                                     \
+  if (a.stats && tid == 0) {                          \
+    const long long now_ = clock64();                 \
+    s_ph[(i)] += now_ - t_sub;                        \
+    t_sub = now_;                                     \
+  }
+#define TF_MARK(i)                                    \
+  if (a.stats && tid == 0) {                          \
+    const long long now_ = clock64();                 \
+    if ((i) > 0) s_ph[(i)] += now_ - t_mark;          \
+    else s_ph[0] += now_ - t_frame0;                  \
+    t_mark = now_;                                    \
+    t_sub = now_;                                     \
+  }
+  long long t_frame0 = 0;
+  if (tid < 32) s_ph[tid] = 0;
   __shared__ long long s_next;
   __shared__ double s_amp;
 
@@ -561,7 +613,7 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
     }
     const int K = a.det.count[f];
     T = s_T;
-    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; }
+    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; t_frame0 = clock64(); }
     for (int k = tid; k < K; k += blockDim.x) {
       for (int q = 0; q < 4; ++q) d_meas[4 * k + q] = a.det.meas[(fK + k) * 4 + q];
       d_obj[k] = a.det.obj[fK + k];
@@ -574,19 +626,18 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
       double* c = &t_cov[12 * t];
       KF::predict(P, m, c);
       t_mdet[t] = -1;
-      if (gating && P.gate_metric == 0) {
-        double sv[4];
-        if (!KF::project(P, m, c, sv, &t_il[4 * t])) flag_error(&s_err, t + 1, TF_NUMERIC);
-      }
     }
     if (tid == 0 && gating && P.gate_metric != 0 && P.gate_metric != 1) flag_error(&s_err, 0, TF_CONFIG);
     __syncthreads();
+    TF_MARK(0);
 
     // ---- gate (tf/tracker.py:109-110, tf/motion.py:128-142) ----------------
     if (gating) {
       for (int t = wid; t < T; t += nw) {
         const double* m = &t_mean[8 * t];
-        const double* il = &t_il[4 * t];
+        double il[4], sv[4];
+        if (P.gate_metric == 0 && !KF::project(P, m, &t_cov[12 * t], sv, il) && lane == 0)
+          flag_error(&s_err, t + 1, TF_NUMERIC);
         int cnt = 0;
         for (int k0 = 0; k0 < K; k0 += 32) {
           const int k = k0 + lane;
@@ -610,6 +661,7 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
       }
     }
     __syncthreads();
+    TF_MARK(1);
     // ---- CSR of finite (un-gated) entries, row-major -----------------------
     if (gating) {
       if (wid == 0) {
@@ -647,6 +699,7 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
         }
       }
       __syncthreads();
+      TF_MARK(2);
       // ---- fp64 cosine cost of un-gated pairs (tf/assoc.py:34-46) ----------
       // fp32 x fp32 products are exact in fp64, so fma == mul + add bit for bit.
       // Two entries per warp iteration keep 16 x 128-bit loads in flight per lane.
@@ -700,32 +753,104 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
       }
     }
     __syncthreads();
+    TF_MARK(3);
     if (s_err != STATUS_CLEAR) {
       if (tid == 0) s_status = (b << 8) | (s_err & 0xff);
       break;
     }
 
-    // ---- exact LAP (tf/assoc.py:60-87), decomposed by connected components --
-    // The padded problem (sentinel everywhere but the finite entries) maximises
-    // the number of finite pairs, then minimises their cost; it separates over
-    // the connected components of the finite bipartite graph whenever the
-    // optimum is unique. Single-edge components are matched directly, larger
-    // components are solved by one warp each with the same exact solver on the
-    // component's submatrix. When a component holds two equal costs (a genuine
-    // tie: e.g. two detections sharing one cell's embedding) the whole padded
-    // matrix is solved by the scipy-order restatement instead, so the tie is
-    // broken exactly as the reference breaks it.
+    // ---- exact LAP (tf/assoc.py:60-87) --------------------------------------
+    // The reference pads the gated matrix with a sentinel and solves it with
+    // scipy's shortest-augmenting-path LAP: maximise the number of finite
+    // pairs, then minimise their cost. Three exact steps:
+    //  1. forced-pair peeling. Two exchange arguments force pairs in EVERY
+    //     optimum: R1 a row whose only live edge (t,c) is the strict minimum
+    //     of column c's live edges; R2 a column whose only live edge (t,c) is
+    //     the strict minimum of row t's live edges. Peeling repeats until
+    //     nothing is forced (edge-parallel, atomics on bit patterns of the
+    //     non-negative costs);
+    //  2. the residual graph (lost tracks with wide gates competing for
+    //     unclaimed detections) is split into connected components; when no
+    //     component holds two equal costs the optimum is unique and each
+    //     component is solved by one warp with the scipy-order restatement;
+    //  3. otherwise (a genuine tie, e.g. two detections sharing one cell's
+    //     embedding) the whole padded matrix is solved by the scipy-order
+    //     restatement, so the tie is broken exactly as the reference breaks it.
     if (gating) {
       const int E = s_E;
       const int NN = T + K;
+      for (int r = tid; r < T; r += blockDim.x) { rcol[r] = -1; p_ra[r] = 1; }
+      for (int c = tid; c < K; c += blockDim.x) { p_ca[c] = 1; c_map[c] = -1; }
+      unsigned long long* p_rminb = reinterpret_cast<unsigned long long*>(p_rmin);
+      // entries beyond the on-chip pool (dense gates): solve the padded matrix directly
+      const bool dense = E > a.cap_entries;
+      for (; !dense;) {
+        for (int c = tid; c < K; c += blockDim.x) { p_cmin[c] = ~0ull; p_ccnt[c] = 0; p_cdeg[c] = 0; }
+        for (int r = tid; r < T; r += blockDim.x) { p_rminb[r] = ~0ull; p_rcnt[r] = 0; p_rdeg[r] = 0; }
+        if (tid == 0) s_flag = 0;
+        __syncthreads();
+        for (int e = tid; e < E; e += blockDim.x) {
+          const int r = erow[e], c = ecol[e];
+          if (p_ra[r] && p_ca[c]) {
+            const unsigned long long bv = static_cast<unsigned long long>(__double_as_longlong(eval[e]));
+            atomicMin(&p_cmin[c], bv);
+            atomicAdd(&p_cdeg[c], 1);
+            p_crow[c] = r;                 // the row, when the degree ends up 1
+            atomicMin(&p_rminb[r], bv);
+            atomicAdd(&p_rdeg[r], 1);
+            p_rc1[r] = c;                  // the column, when the degree ends up 1
+          }
+        }
+        __syncthreads();
+        for (int e = tid; e < E; e += blockDim.x) {
+          const int r = erow[e], c = ecol[e];
+          if (p_ra[r] && p_ca[c]) {
+            const unsigned long long bv = static_cast<unsigned long long>(__double_as_longlong(eval[e]));
+            if (bv == p_cmin[c]) atomicAdd(&p_ccnt[c], 1);
+            if (bv == p_rminb[r]) atomicAdd(&p_rcnt[r], 1);
+          }
+        }
+        __syncthreads();
+        for (int r = tid; r < T; r += blockDim.x)        // R1
+          if (p_ra[r] && p_rdeg[r] == 1) {
+            const int c = p_rc1[r];
+            if (p_ccnt[c] == 1 && p_rminb[r] == p_cmin[c]) {
+              rcol[r] = static_cast<int16_t>(c);
+              p_kr[r] = 1;
+              p_kc[c] = 1;
+              s_flag = 1;
+            }
+          }
+        for (int c = tid; c < K; c += blockDim.x)        // R2
+          if (p_ca[c] && p_cdeg[c] == 1) {
+            const int r = p_crow[c];
+            if (p_rcnt[r] == 1 && p_rminb[r] == p_cmin[c]) {
+              rcol[r] = static_cast<int16_t>(c);
+              p_kr[r] = 1;
+              p_kc[c] = 1;
+              s_flag = 1;
+            }
+          }
+        __syncthreads();
+        const int go = s_flag;
+        for (int r = tid; r < T; r += blockDim.x) if (p_kr[r]) { p_ra[r] = 0; p_kr[r] = 0; }
+        for (int c = tid; c < K; c += blockDim.x) if (p_kc[c]) { p_ca[c] = 0; p_kc[c] = 0; }
+        __syncthreads();
+        if (!go) break;
+      }
+      TF_SUB(17);
+      // residual edges, compacted in CSR order
+      const int E_live = dense ? 0 : block_rank(E, [&](int e) { return p_ra[erow[e]] && p_ca[ecol[e]]; }, c_epos, s_warp);
+      if (!dense)
+        for (int e = tid; e < E; e += blockDim.x)
+          if (c_epos[e] >= 0) c_elist[c_epos[e]] = static_cast<int16_t>(e);
       for (int x = tid; x < NN; x += blockDim.x) {
         c_lab[x] = x;
         c_nr[x] = 0;
         c_nc[x] = 0;
         c_ne[x] = 0;
       }
-      for (int t = tid; t < T; t += blockDim.x) rcol[t] = -1;
-      if (tid == 0) { s_flag = 1; s_tie = (E > 1024); }
+      if (tid == 0) { s_flag = 1; s_tie = dense; }
       for (;;) {
         __syncthreads();
         const int go = s_flag;
@@ -733,7 +858,8 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
         if (!go) break;
         if (tid == 0) s_flag = 0;
         __syncthreads();
-        for (int e = tid; e < E; e += blockDim.x) {
+        for (int q = tid; q < E_live; q += blockDim.x) {
+          const int e = c_elist[q];
           const int r = erow[e], c = T + ecol[e];
           const int la = c_lab[r], lb = c_lab[c];
           if (la != lb) {
@@ -749,39 +875,42 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
           if (ll < l) c_lab[x] = ll;
         }
       }
-      for (int x = tid; x < NN; x += blockDim.x) atomicAdd(x < T ? &c_nr[c_lab[x]] : &c_nc[c_lab[x]], 1);
-      for (int e = tid; e < E; e += blockDim.x) {
+      for (int x = tid; x < NN; x += blockDim.x) {
+        const bool alive = x < T ? p_ra[x] != 0 : p_ca[x - T] != 0;
+        if (alive) atomicAdd(x < T ? &c_nr[c_lab[x]] : &c_nc[c_lab[x]], 1);
+      }
+      for (int q = tid; q < E_live; q += blockDim.x) {
+        const int e = c_elist[q];
         const int root = c_lab[erow[e]];
         atomicAdd(&c_ne[root], 1);
-        if (!s_tie) {
-          const double v0 = eval[e];
-          for (int e2 = e + 1; e2 < E; ++e2)
-            if (eval[e2] == v0 && c_lab[erow[e2]] == root) { s_tie = 1; break; }
+        const double v0 = eval[e];
+        for (int q2 = q + 1; q2 < E_live && !s_tie; ++q2) {
+          const int e2 = c_elist[q2];
+          if (eval[e2] == v0 && c_lab[erow[e2]] == root) s_tie = 1;
         }
       }
       __syncthreads();
+      TF_SUB(16);
+      if (a.stats && tid == 0) { s_ph[8] += s_tie; s_ph[9] += E; s_ph[11] += 1; s_ph[12] += T; s_ph[13] += K; s_ph[14] += E_live; }
       if (s_tie) {
         if (wid == 0) {
           const int n = T > K ? T : K;
           const double sentinel = 2.0 * static_cast<double>(n) * fmax(s_amp, 1.0) + 1.0;
           warp_lap(n, T, CsrRows{rowptr, ecol, eval}, sentinel, L);
           __syncwarp();
-          for (int t = lane; t < T; t += 32) {
-            const int c = L.col4row[t];
-            rcol[t] = static_cast<int16_t>(c < K ? c : -1);
+          for (int r = lane; r < T; r += 32) {
+            const int c = L.col4row[r];
+            rcol[r] = static_cast<int16_t>(c < K ? c : -1);
           }
+          TF_SUB(20);
         }
       } else {
-        // single-edge components
-        for (int e = tid; e < E; e += blockDim.x) {
-          const int root = c_lab[erow[e]];
-          if (c_nr[root] == 1 && c_nc[root] == 1) rcol[erow[e]] = ecol[e];
-        }
-        // multi-edge components: ordered list, scratch slices, one warp each
-        const int n_multi = block_rank(NN, [&](int x) { return c_lab[x] == x && c_ne[x] >= 2; }, c_pos, s_warp);
+        const int n_multi = block_rank(NN, [&](int x) { return c_lab[x] == x && c_ne[x] >= 1; }, c_pos, s_warp);
+        if (a.stats && tid == 0) s_ph[10] += n_multi;
         for (int x = tid; x < NN; x += blockDim.x)
           if (c_pos[x] >= 0) c_root[c_pos[x]] = x;
         __syncthreads();
+        TF_SUB(18);
         if (wid == 0) {
           int carry = 0;
           for (int i0 = 0; i0 < n_multi; i0 += 32) {
@@ -804,14 +933,14 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
           int nr_l = 0, nc_l = 0;
           for (int t0 = 0; t0 < T; t0 += 32) {
             const int t = t0 + lane;
-            const bool in = t < T && c_lab[t] == root;
+            const bool in = t < T && c_lab[t] == root && p_ra[t];
             const unsigned bm = __ballot_sync(FULL, in);
             if (in) c_rows[off + nr_l + __popc(bm & ((1u << lane) - 1u))] = static_cast<int16_t>(t);
             nr_l += __popc(bm);
           }
           for (int k0 = 0; k0 < K; k0 += 32) {
             const int k = k0 + lane;
-            const bool in = k < K && c_lab[T + k] == root;
+            const bool in = k < K && c_lab[T + k] == root && p_ca[k];
             const unsigned bm = __ballot_sync(FULL, in);
             if (in) {
               const int j = nc_l + __popc(bm & ((1u << lane) - 1u));
@@ -841,6 +970,29 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
       }
     }
     __syncthreads();
+    TF_SUB(19);
+    TF_MARK(4);
+    // ---- matches + max_cost threshold (tf/assoc.py:77-107) -----------------
+    if (gating) {
+      for (int t = tid; t < T; t += blockDim.x) {
+        const int c = rcol[t];
+        int md = -1;
+        double mc = 0.0;
+        if (c >= 0) {
+          for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
+            if (ecol[e] == c) {
+              mc = eval[e];
+              md = (mc > P.max_cost) ? -1 : c;
+              break;
+            }
+        }
+        t_mdet[t] = md;
+        t_mcost[t] = mc;
+        if (md >= 0) d_row[md] = t;
+      }
+    }
+    __syncthreads();
+    TF_MARK(5);
     // ---- matched: Kalman update + lifecycle (tf/tracker.py:114-125) --------
     for (int t = tid; t < T; t += blockDim.x) {
       const int k = t_mdet[t];
@@ -884,6 +1036,7 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
       }
     }
     __syncthreads();
+    TF_MARK(6);
 
     // ---- records: matched tracks in list (= id) order, then births ---------
     // Births are unmatched detections in ascending order (tf/tracker.py:145-157).
@@ -985,6 +1138,7 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
         }
       }
       __syncthreads();
+      TF_MARK(7);
       // copy detection embeddings into the new tracks' slots (warp per birth)
       for (int k = wid; k < K; k += nw) {
         const int r = d_pos[k];
@@ -1024,6 +1178,8 @@ __global__ void __launch_bounds__(kAssocThreads) associate_kernel(AssocArgs a, P
     for (int q = 0; q < 8; ++q) tb.mean[(sT + t) * 8 + q] = t_mean[8 * t + q];
     for (int q = 0; q < 12; ++q) tb.cov[(sT + t) * 12 + q] = t_cov[12 * t + q];
   }
+  if (a.stats && tid < 32) atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[tid]),
+                                      static_cast<unsigned long long>(s_ph[tid]));
   if (tid == 0) {
     tb.n_tracks[s] = T;
     tb.next_id[s] = s_next;

@@ -66,6 +66,7 @@ struct AssocArgs {
   int16_t* pool_col;             // [streams][cap_tracks * cap_det] overflow CSR
   int16_t* pool_row;
   double* pool_val;
+  long long* stats;              // [16] phase cycles / counters (nullptr = off)
 };
 
 struct HeadLaunch {
