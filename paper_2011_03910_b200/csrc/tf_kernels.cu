@@ -407,7 +407,7 @@ struct AssocPlan {
       off_slot, off_mdet, off_rowptr, off_flag, off_npos, off_rpos, off_dm, off_dobj, off_drow, off_dpos, off_gmask,
       off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
       off_vr, off_vc, off_lab, off_cnr, off_cnc, off_cne, off_croot, off_coff, off_cpos, off_crows, off_ccols,
-      off_cmap, off_rcol, off_epos, off_elist, off_pcmin, off_prmin, off_pccnt, off_pcdeg, off_pcrow, off_prdeg, off_prcnt, off_prc1,
+      off_cmap, off_rcol, off_il, off_epos, off_elist, off_pcmin, off_prmin, off_pccnt, off_pcdeg, off_pcrow, off_prdeg, off_prcnt, off_prc1,
       off_pra, off_pca, off_pkr, off_pkc, total;
 };
 
@@ -453,6 +453,7 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   // built) shares this region
   const size_t ustart = o;
   p.off_gmask = ustart;
+  p.off_il = align16(ustart + 4 * T * KW);
   TF_TAKE(off_lab, 4 * NN)
   TF_TAKE(off_cnr, 4 * NN)
   TF_TAKE(off_cnc, 4 * NN)
@@ -479,7 +480,7 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_pca, K)
   TF_TAKE(off_pkr, T)
   TF_TAKE(off_pkc, K)
-  if (o < align16(ustart + 4 * T * KW)) o = align16(ustart + 4 * T * KW);
+  if (o < align16(p.off_il + 32 * T)) o = align16(p.off_il + 32 * T);
 #undef TF_TAKE
   p.total = o;
   return p;
@@ -512,6 +513,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   int* d_row = reinterpret_cast<int*>(smem + pl.off_drow);
   int16_t* d_pos = reinterpret_cast<int16_t*>(smem + pl.off_dpos);
   unsigned* gmask = reinterpret_cast<unsigned*>(smem + pl.off_gmask);
+  double* g_il = reinterpret_cast<double*>(smem + pl.off_il);   // 1/sqrt(S_i) per track (gate phase)
   LapScratch L;
   L.u = reinterpret_cast<double*>(smem + pl.off_u);
   L.v = reinterpret_cast<double*>(smem + pl.off_v);
@@ -552,7 +554,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   for (int x = threadIdx.x; x < Km; x += blockDim.x) p_kc[x] = 0;
 
   __shared__ int s_warp[33];
-  __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie;
+  __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work;
   // optional phase timing (tf_set_profiling): cycles per phase + counters
   __shared__ long long s_ph[32];
   long long t_mark = 0, t_sub = 0;
@@ -613,7 +615,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     }
     const int K = a.det.count[f];
     T = s_T;
-    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; t_frame0 = clock64(); }
+    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; s_work = 0; t_frame0 = clock64(); }
     for (int k = tid; k < K; k += blockDim.x) {
       for (int q = 0; q < 4; ++q) d_meas[4 * k + q] = a.det.meas[(fK + k) * 4 + q];
       d_obj[k] = a.det.obj[fK + k];
@@ -626,6 +628,11 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       double* c = &t_cov[12 * t];
       KF::predict(P, m, c);
       t_mdet[t] = -1;
+      t_flag[t] = 0;
+      if (gating && P.gate_metric == 0) {
+        double sv[4];
+        if (!KF::project(P, m, c, sv, &g_il[4 * t])) flag_error(&s_err, t + 1, TF_NUMERIC);
+      }
     }
     if (tid == 0 && gating && P.gate_metric != 0 && P.gate_metric != 1) flag_error(&s_err, 0, TF_CONFIG);
     __syncthreads();
@@ -633,31 +640,29 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
 
     // ---- gate (tf/tracker.py:109-110, tf/motion.py:128-142) ----------------
     if (gating) {
-      for (int t = wid; t < T; t += nw) {
+      // one warp per (track, 32-detection chunk): balanced over the CTA
+      const int KC = (K + 31) >> 5;
+      for (int it = wid; it < T * KC; it += nw) {
+        const int t = it / KC, k0 = (it - t * KC) << 5;
+        const int k = k0 + lane;
         const double* m = &t_mean[8 * t];
-        double il[4], sv[4];
-        if (P.gate_metric == 0 && !KF::project(P, m, &t_cov[12 * t], sv, il) && lane == 0)
-          flag_error(&s_err, t + 1, TF_NUMERIC);
-        int cnt = 0;
-        for (int k0 = 0; k0 < K; k0 += 32) {
-          const int k = k0 + lane;
-          bool fin = false;
-          if (k < K) {
-            const double* z = &d_meas[4 * k];
-            double g;
-            if (P.gate_metric == 0) {
-              g = KF::mahalanobis(m, il, z);
-            } else {
-              double dx = m[0] - z[0], dy = m[1] - z[1];
-              g = dx * dx + dy * dy;
-            }
-            fin = !(g > P.gate_threshold);
+        bool fin = false;
+        if (k < K) {
+          const double* z = &d_meas[4 * k];
+          double g;
+          if (P.gate_metric == 0) {
+            g = KF::mahalanobis(m, &g_il[4 * t], z);
+          } else {
+            double dx = m[0] - z[0], dy = m[1] - z[1];
+            g = dx * dx + dy * dy;
           }
-          unsigned bm = __ballot_sync(FULL, fin);
-          if (lane == 0) gmask[t * KW + (k0 >> 5)] = bm;
-          cnt += __popc(bm);
+          fin = !(g > P.gate_threshold);
         }
-        if (lane == 0) t_flag[t] = cnt;
+        const unsigned bm = __ballot_sync(FULL, fin);
+        if (lane == 0) {
+          gmask[t * KW + (k0 >> 5)] = bm;
+          if (bm) atomicAdd(&t_flag[t], __popc(bm));
+        }
       }
     }
     __syncthreads();
@@ -702,8 +707,57 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       TF_MARK(2);
       // ---- fp64 cosine cost of un-gated pairs (tf/assoc.py:34-46) ----------
       // fp32 x fp32 products are exact in fp64, so fma == mul + add bit for bit.
-      // Two entries per warp iteration keep 16 x 128-bit loads in flight per lane.
+      // D = 512: rows are handed to warps by an atomic counter; the track's
+      // embedding stays in registers while its (few) detections stream by,
+      // two at a time. Other D: two entries per warp iteration.
       double amp = 0.0;
+      if (D == 512) {
+        for (;;) {
+          int t = 0;
+          if (lane == 0) t = atomicAdd(&s_work, 1);
+          t = __shfl_sync(FULL, t, 0);
+          if (t >= T) break;
+          const int e0 = rowptr[t], e1 = rowptr[t + 1];
+          if (e0 == e1) continue;
+          const float4* t4 = reinterpret_cast<const float4*>(a.trk.emb_pool + (sT + t_slot[t]) * 512ll);
+          float4 x[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = t4[lane + 32 * q];
+          for (int e = e0; e < e1; e += 2) {
+            const bool two = e + 1 < e1;
+            const float4* d0 = reinterpret_cast<const float4*>(a.det.emb + (fK + ecol[e]) * 512ll);
+            const float4* d1 = reinterpret_cast<const float4*>(a.det.emb + (fK + ecol[two ? e + 1 : e]) * 512ll);
+            float4 y0[4], y1[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { y0[q] = d0[lane + 32 * q]; y1[q] = d1[lane + 32 * q]; }
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              acc0 = fma(static_cast<double>(x[q].x), static_cast<double>(y0[q].x), acc0);
+              acc1 = fma(static_cast<double>(x[q].x), static_cast<double>(y1[q].x), acc1);
+              acc0 = fma(static_cast<double>(x[q].y), static_cast<double>(y0[q].y), acc0);
+              acc1 = fma(static_cast<double>(x[q].y), static_cast<double>(y1[q].y), acc1);
+              acc0 = fma(static_cast<double>(x[q].z), static_cast<double>(y0[q].z), acc0);
+              acc1 = fma(static_cast<double>(x[q].z), static_cast<double>(y1[q].z), acc1);
+              acc0 = fma(static_cast<double>(x[q].w), static_cast<double>(y0[q].w), acc0);
+              acc1 = fma(static_cast<double>(x[q].w), static_cast<double>(y1[q].w), acc1);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              acc0 += __shfl_xor_sync(FULL, acc0, o);
+              acc1 += __shfl_xor_sync(FULL, acc1, o);
+            }
+            const double c0 = fmin(fmax(1.0 - acc0, 0.0), 2.0);
+            const double c1 = fmin(fmax(1.0 - acc1, 0.0), 2.0);
+            if (lane == 0) {
+              eval[e] = c0;
+              if (two) eval[e + 1] = c1;
+            }
+            amp = fmax(amp, c0);
+            if (two) amp = fmax(amp, c1);
+          }
+        }
+      } else
       for (int e0 = 2 * wid; e0 < E; e0 += 2 * nw) {
         const bool two = e0 + 1 < E;
         const int e1 = two ? e0 + 1 : e0;
@@ -1013,16 +1067,52 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       }
       t_flag[t] = remove;
     }
-    // EMA appearance update, one warp per matched track (tf/tracker.py:67-71, 117-119)
-    for (int t = wid; t < T; t += nw) {
-      const int k = t_mdet[t];
-      if (k < 0) continue;
+    // EMA appearance update, one warp per matched detection (tf/tracker.py:67-71,
+    // 117-119): normalize(alpha * old + (1 - alpha) * new) in fp64, fp32 out.
+    for (int k = wid; k < K; k += nw) {
+      const int t = d_row[k];
+      if (t < 0) continue;
       float* te = a.trk.emb_pool + (sT + t_slot[t]) * static_cast<long long>(D);
       const float* de = a.det.emb + (fK + k) * static_cast<long long>(D);
+      if (D == 512) {                                   // one pass, rows held in registers
+        const float4* t4 = reinterpret_cast<const float4*>(te);
+        const float4* d4 = reinterpret_cast<const float4*>(de);
+        float4 x[4], y[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { x[q] = t4[lane + 32 * q]; y[q] = d4[lane + 32 * q]; }
+        double v[16];
+        double ss = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[4 * q + 0] = P.alpha * static_cast<double>(x[q].x) + P.beta * static_cast<double>(y[q].x);
+          v[4 * q + 1] = P.alpha * static_cast<double>(x[q].y) + P.beta * static_cast<double>(y[q].y);
+          v[4 * q + 2] = P.alpha * static_cast<double>(x[q].z) + P.beta * static_cast<double>(y[q].z);
+          v[4 * q + 3] = P.alpha * static_cast<double>(x[q].w) + P.beta * static_cast<double>(y[q].w);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) ss = fma(v[q], v[q], ss);
+        ss = warp_sum(ss);
+        const double nrm = sqrt(ss);
+        if (!(nrm >= 1e-12) || !isfinite(nrm)) {
+          if (lane == 0) flag_error(&s_err, t + 1, TF_DEGENERATE_EMBEDDING);
+          continue;
+        }
+        float4* o4 = reinterpret_cast<float4*>(te);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float4 r;
+          r.x = static_cast<float>(v[4 * q + 0] / nrm);
+          r.y = static_cast<float>(v[4 * q + 1] / nrm);
+          r.z = static_cast<float>(v[4 * q + 2] / nrm);
+          r.w = static_cast<float>(v[4 * q + 3] / nrm);
+          o4[lane + 32 * q] = r;
+        }
+        continue;
+      }
       double ss = 0.0;
       for (int i = lane; i < D; i += 32) {
         double v = P.alpha * static_cast<double>(te[i]) + P.beta * static_cast<double>(de[i]);
-        ss += v * v;
+        ss = fma(v, v, ss);
       }
       ss = warp_sum(ss);
       double nrm = sqrt(ss);
@@ -1030,6 +1120,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         if (lane == 0) flag_error(&s_err, t + 1, TF_DEGENERATE_EMBEDDING);
         continue;
       }
+      __syncwarp();
       for (int i = lane; i < D; i += 32) {
         double v = P.alpha * static_cast<double>(te[i]) + P.beta * static_cast<double>(de[i]);
         te[i] = static_cast<float>(v / nrm);
