@@ -9,6 +9,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -52,6 +53,7 @@ struct tf_ctx {
   size_t events_used;
   long long prof_bytes_frame, prof_frames;
   long long* d_stats;
+  int cluster_key, cluster_val;   // cached cluster size for the last stream count
   std::vector<void*> allocs;
 };
 
@@ -231,6 +233,8 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   c->events_used = 0;
   c->prof_bytes_frame = 0;
   c->prof_frames = 0;
+  c->cluster_key = -1;
+  c->cluster_val = 1;
   for (int i = 0; i < 3; ++i) {
     c->stage_conf[i] = nullptr;
     c->stage_conf_elems[i] = 0;
@@ -442,6 +446,15 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
   a.stats = c->profiling ? c->d_stats : nullptr;
+  {
+    const char* env = getenv("TF_CLUSTER");
+    const int key = n_streams * 64 + (env ? atoi(env) & 63 : 0);
+    if (key != c->cluster_key) {
+      c->cluster_val = assoc_cluster_size(n_streams, a.cap_tracks, a.cap_det, a.cap_entries);
+      c->cluster_key = key;
+    }
+    a.cluster = c->cluster_val;
+  }
   const bool host_out = heads->host_memory != 0;
   if (host_out) {
     rc = ensure_record_staging(c, F, out->max_records);
@@ -508,6 +521,7 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
   a.stats = c->profiling ? c->d_stats : nullptr;
+  a.cluster = 1;
   a.out.count = out->count;
   a.out.track_id = reinterpret_cast<long long*>(out->track_id);
   a.out.box = out->box;

@@ -14,7 +14,11 @@
 //  stage kernels        batched nms / lap / kalman / gating / cost / normalize /
 //                       binary16 / smooth / iou for the reference's module-level
 //                       functions.
+#include <cooperative_groups.h>
+
 #include "tf_kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace tfd {
 
@@ -486,10 +490,175 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   return p;
 }
 
+
+// ---- cluster-cooperative phases of associate_kernel ----------------------------
+// The association of one stream is sequential per frame, but two of its phases
+// are embarrassingly parallel and L2-latency bound: the fp64 cosine costs of the
+// un-gated pairs and the EMA appearance updates. With a thread-block cluster per
+// stream, follower CTAs join exactly these phases: work is handed out through
+// an atomic counter in the leader's shared memory (DSMEM), and results are
+// written back into it. Views carry leader-local or DSMEM-mapped pointers.
+struct CostView {
+  const int* rowptr;
+  const int16_t* ecol;
+  const int16_t* erow;
+  double* eval;
+  const int* t_slot;
+  int* work;
+  unsigned long long* amp;     // bit pattern of the (non-negative) max cost
+  const float* pool;           // this stream's embedding pool
+  const float* dets;           // this frame's detection embeddings
+  int T, E, D;
+};
+
+__device__ void cost_work(const CostView v, int worker, int n_workers) {
+  // Entry pairs are statically partitioned over every warp of the cluster
+  // (worker = global warp index): no atomics on the critical path, and each
+  // warp keeps 2 x 2 KB x 2 rows of 128-bit loads in flight per pair.
+  const int lane = lane_id();
+  double amp = 0.0;
+  for (int e0 = 2 * worker; e0 < v.E; e0 += 2 * n_workers) {
+    const bool two = e0 + 1 < v.E;
+    const int e1 = two ? e0 + 1 : e0;
+    const int r0 = v.erow[e0], r1 = v.erow[e1];
+    const int k0 = v.ecol[e0], k1 = v.ecol[e1];
+    const float* te0 = v.pool + static_cast<long long>(v.t_slot[r0]) * v.D;
+    const float* te1 = v.pool + static_cast<long long>(v.t_slot[r1]) * v.D;
+    const float* de0 = v.dets + static_cast<long long>(k0) * v.D;
+    const float* de1 = v.dets + static_cast<long long>(k1) * v.D;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (v.D == 512) {
+      const float4 *x0 = reinterpret_cast<const float4*>(te0), *y0 = reinterpret_cast<const float4*>(de0);
+      const float4 *x1 = reinterpret_cast<const float4*>(te1), *y1 = reinterpret_cast<const float4*>(de1);
+      float4 a0[4], b0[4], a1[4], b1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a0[q] = x0[lane + 32 * q];
+        b0[q] = y0[lane + 32 * q];
+        a1[q] = x1[lane + 32 * q];
+        b1[q] = y1[lane + 32 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc0 = fma(static_cast<double>(a0[q].x), static_cast<double>(b0[q].x), acc0);
+        acc1 = fma(static_cast<double>(a1[q].x), static_cast<double>(b1[q].x), acc1);
+        acc0 = fma(static_cast<double>(a0[q].y), static_cast<double>(b0[q].y), acc0);
+        acc1 = fma(static_cast<double>(a1[q].y), static_cast<double>(b1[q].y), acc1);
+        acc0 = fma(static_cast<double>(a0[q].z), static_cast<double>(b0[q].z), acc0);
+        acc1 = fma(static_cast<double>(a1[q].z), static_cast<double>(b1[q].z), acc1);
+        acc0 = fma(static_cast<double>(a0[q].w), static_cast<double>(b0[q].w), acc0);
+        acc1 = fma(static_cast<double>(a1[q].w), static_cast<double>(b1[q].w), acc1);
+      }
+    } else {
+      for (int i = lane; i < v.D; i += 32) {
+        acc0 = fma(static_cast<double>(te0[i]), static_cast<double>(de0[i]), acc0);
+        acc1 = fma(static_cast<double>(te1[i]), static_cast<double>(de1[i]), acc1);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc0 += __shfl_xor_sync(FULL, acc0, o);
+      acc1 += __shfl_xor_sync(FULL, acc1, o);
+    }
+    const double c0 = fmin(fmax(1.0 - acc0, 0.0), 2.0);
+    const double c1 = fmin(fmax(1.0 - acc1, 0.0), 2.0);
+    if (lane == 0) {
+      v.eval[e0] = c0;
+      if (two) v.eval[e1] = c1;
+    }
+    amp = fmax(amp, c0);
+    if (two) amp = fmax(amp, c1);
+  }
+  // amplitude = max |finite| (tf/assoc.py:71); costs are >= 0, so an integer
+  // max over the bit patterns is exact
+  if (lane == 0 && amp > 0.0)
+    atomicMax(v.amp, static_cast<unsigned long long>(__double_as_longlong(amp)));
+}
+
+struct EmaView {
+  const int* d_row;            // matched track row of each detection, -1 if none
+  const int* t_slot;
+  int* work;
+  int* err;
+  float* pool;
+  const float* dets;
+  double alpha, beta;
+  int K, D;
+};
+
+// EMA appearance update (tf/tracker.py:67-71, 117-119): one warp per matched
+// detection, normalize(alpha * old + (1 - alpha) * new) in fp64, fp32 out.
+__device__ void ema_work(const EmaView v) {
+  const int lane = lane_id();
+  for (;;) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(v.work, 1);
+    k = __shfl_sync(FULL, k, 0);
+    if (k >= v.K) break;
+    const int t = v.d_row[k];
+    if (t < 0) continue;
+    float* te = v.pool + static_cast<long long>(v.t_slot[t]) * v.D;
+    const float* de = v.dets + static_cast<long long>(k) * v.D;
+    if (v.D == 512) {                                   // one pass, rows held in registers
+      const float4* t4 = reinterpret_cast<const float4*>(te);
+      const float4* d4 = reinterpret_cast<const float4*>(de);
+      float4 x[4], y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { x[q] = t4[lane + 32 * q]; y[q] = d4[lane + 32 * q]; }
+      double w[16];
+      double ss = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        w[4 * q + 0] = v.alpha * static_cast<double>(x[q].x) + v.beta * static_cast<double>(y[q].x);
+        w[4 * q + 1] = v.alpha * static_cast<double>(x[q].y) + v.beta * static_cast<double>(y[q].y);
+        w[4 * q + 2] = v.alpha * static_cast<double>(x[q].z) + v.beta * static_cast<double>(y[q].z);
+        w[4 * q + 3] = v.alpha * static_cast<double>(x[q].w) + v.beta * static_cast<double>(y[q].w);
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) ss = fma(w[q], w[q], ss);
+      ss = warp_sum(ss);
+      const double nrm = sqrt(ss);
+      if (!(nrm >= 1e-12) || !isfinite(nrm)) {
+        if (lane == 0) flag_error(v.err, t + 1, TF_DEGENERATE_EMBEDDING);
+        continue;
+      }
+      float4* o4 = reinterpret_cast<float4*>(te);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float4 r;
+        r.x = static_cast<float>(w[4 * q + 0] / nrm);
+        r.y = static_cast<float>(w[4 * q + 1] / nrm);
+        r.z = static_cast<float>(w[4 * q + 2] / nrm);
+        r.w = static_cast<float>(w[4 * q + 3] / nrm);
+        o4[lane + 32 * q] = r;
+      }
+      continue;
+    }
+    double ss = 0.0;
+    for (int i = lane; i < v.D; i += 32) {
+      double w = v.alpha * static_cast<double>(te[i]) + v.beta * static_cast<double>(de[i]);
+      ss = fma(w, w, ss);
+    }
+    ss = warp_sum(ss);
+    const double nrm = sqrt(ss);
+    if (!(nrm >= 1e-12) || !isfinite(nrm)) {
+      if (lane == 0) flag_error(v.err, t + 1, TF_DEGENERATE_EMBEDDING);
+      continue;
+    }
+    __syncwarp();
+    for (int i = lane; i < v.D; i += 32) {
+      double w = v.alpha * static_cast<double>(te[i]) + v.beta * static_cast<double>(de[i]);
+      te[i] = static_cast<float>(w / nrm);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int ls = blockIdx.x;                 // local stream in this update
+  const int C = a.cluster;                   // CTAs per stream (thread-block cluster)
+  const int ls = blockIdx.x / C;             // local stream in this update
   const int s = a.stream_begin + ls;         // global stream id
+  const int rank = C > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
   const int Tm = a.cap_tracks, Km = a.cap_det, D = P.dim;
   const int KW = (Km + 31) / 32;
@@ -554,7 +723,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   for (int x = threadIdx.x; x < Km; x += blockDim.x) p_kc[x] = 0;
 
   __shared__ int s_warp[33];
-  __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work;
+  __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work, s_Efr, s_emaK, s_cmd;
   // optional phase timing (tf_set_profiling): cycles per phase + counters
   __shared__ long long s_ph[32];
   long long t_mark = 0, t_sub = 0;
@@ -582,6 +751,60 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   int16_t* erow = reinterpret_cast<int16_t*>(smem + pl.off_erow);
   double* eval = reinterpret_cast<double*>(smem + pl.off_eval);
 
+  if (rank != 0) {
+    // ---- follower CTA: joins the cost and EMA phases of every frame -------
+    cg::cluster_group cl = cg::this_cluster();
+    const int* L_cmd = cl.map_shared_rank(&s_cmd, 0);
+    const int* L_T = cl.map_shared_rank(&s_T, 0);
+    const int* L_E = cl.map_shared_rank(&s_Efr, 0);
+    const int* L_K = cl.map_shared_rank(&s_emaK, 0);
+    const long long sTf = static_cast<long long>(s) * Tm;
+    for (int b = 0;; ++b) {
+      cl.sync();                                                      // S1
+      if (*L_cmd) {
+        cl.sync();
+        return;
+      }
+      const long long fKf = static_cast<long long>(ls * a.B + b) * Km;
+      const int E = *L_E;
+      if (E > 0) {
+        CostView cv;
+        const bool pooled = E > a.cap_entries;
+        cv.rowptr = cl.map_shared_rank(rowptr, 0);
+        cv.ecol = pooled ? a.pool_col + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(ecol, 0);
+        cv.erow = pooled ? a.pool_row + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(erow, 0);
+        cv.eval = pooled ? a.pool_val + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(eval, 0);
+        cv.t_slot = cl.map_shared_rank(t_slot, 0);
+        cv.work = cl.map_shared_rank(&s_work, 0);
+        cv.amp = reinterpret_cast<unsigned long long*>(cl.map_shared_rank(&s_amp, 0));
+        cv.pool = a.trk.emb_pool + sTf * static_cast<long long>(D);
+        cv.dets = a.det.emb + fKf * static_cast<long long>(D);
+        cv.T = *L_T;
+        cv.E = E;
+        cv.D = D;
+        cost_work(cv, rank * n_warps() + warp_id(), n_warps() * C);
+      }
+      cl.sync();                                                      // S2
+      cl.sync();                                                      // S3
+      const int Ke = *L_K;
+      if (Ke > 0) {
+        EmaView ev;
+        ev.d_row = cl.map_shared_rank(d_row, 0);
+        ev.t_slot = cl.map_shared_rank(t_slot, 0);
+        ev.work = cl.map_shared_rank(&s_work, 0);
+        ev.err = cl.map_shared_rank(&s_err, 0);
+        ev.pool = a.trk.emb_pool + sTf * static_cast<long long>(D);
+        ev.dets = a.det.emb + fKf * static_cast<long long>(D);
+        ev.alpha = P.alpha;
+        ev.beta = P.beta;
+        ev.K = Ke;
+        ev.D = D;
+        ema_work(ev);
+      }
+      cl.sync();                                                      // S4
+    }
+  }
+  if (tid == 0) s_cmd = 0;
   TrackBuf& tb = a.trk;
   const long long sT = static_cast<long long>(s) * Tm;
   if (tid == 0) {
@@ -615,7 +838,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     }
     const int K = a.det.count[f];
     T = s_T;
-    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; s_work = 0; t_frame0 = clock64(); }
+    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; s_work = 0; s_Efr = 0; t_frame0 = clock64(); }
     for (int k = tid; k < K; k += blockDim.x) {
       for (int q = 0; q < 4; ++q) d_meas[4 * k + q] = a.det.meas[(fK + k) * 4 + q];
       d_obj[k] = a.det.obj[fK + k];
@@ -705,113 +928,34 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       }
       __syncthreads();
       TF_MARK(2);
-      // ---- fp64 cosine cost of un-gated pairs (tf/assoc.py:34-46) ----------
-      // fp32 x fp32 products are exact in fp64, so fma == mul + add bit for bit.
-      // D = 512: rows are handed to warps by an atomic counter; the track's
-      // embedding stays in registers while its (few) detections stream by,
-      // two at a time. Other D: two entries per warp iteration.
-      double amp = 0.0;
-      if (D == 512) {
-        for (;;) {
-          int t = 0;
-          if (lane == 0) t = atomicAdd(&s_work, 1);
-          t = __shfl_sync(FULL, t, 0);
-          if (t >= T) break;
-          const int e0 = rowptr[t], e1 = rowptr[t + 1];
-          if (e0 == e1) continue;
-          const float4* t4 = reinterpret_cast<const float4*>(a.trk.emb_pool + (sT + t_slot[t]) * 512ll);
-          float4 x[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) x[q] = t4[lane + 32 * q];
-          for (int e = e0; e < e1; e += 2) {
-            const bool two = e + 1 < e1;
-            const float4* d0 = reinterpret_cast<const float4*>(a.det.emb + (fK + ecol[e]) * 512ll);
-            const float4* d1 = reinterpret_cast<const float4*>(a.det.emb + (fK + ecol[two ? e + 1 : e]) * 512ll);
-            float4 y0[4], y1[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) { y0[q] = d0[lane + 32 * q]; y1[q] = d1[lane + 32 * q]; }
-            double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              acc0 = fma(static_cast<double>(x[q].x), static_cast<double>(y0[q].x), acc0);
-              acc1 = fma(static_cast<double>(x[q].x), static_cast<double>(y1[q].x), acc1);
-              acc0 = fma(static_cast<double>(x[q].y), static_cast<double>(y0[q].y), acc0);
-              acc1 = fma(static_cast<double>(x[q].y), static_cast<double>(y1[q].y), acc1);
-              acc0 = fma(static_cast<double>(x[q].z), static_cast<double>(y0[q].z), acc0);
-              acc1 = fma(static_cast<double>(x[q].z), static_cast<double>(y1[q].z), acc1);
-              acc0 = fma(static_cast<double>(x[q].w), static_cast<double>(y0[q].w), acc0);
-              acc1 = fma(static_cast<double>(x[q].w), static_cast<double>(y1[q].w), acc1);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              acc0 += __shfl_xor_sync(FULL, acc0, o);
-              acc1 += __shfl_xor_sync(FULL, acc1, o);
-            }
-            const double c0 = fmin(fmax(1.0 - acc0, 0.0), 2.0);
-            const double c1 = fmin(fmax(1.0 - acc1, 0.0), 2.0);
-            if (lane == 0) {
-              eval[e] = c0;
-              if (two) eval[e + 1] = c1;
-            }
-            amp = fmax(amp, c0);
-            if (two) amp = fmax(amp, c1);
-          }
-        }
-      } else
-      for (int e0 = 2 * wid; e0 < E; e0 += 2 * nw) {
-        const bool two = e0 + 1 < E;
-        const int e1 = two ? e0 + 1 : e0;
-        const float* te0 = a.trk.emb_pool + (sT + t_slot[erow[e0]]) * static_cast<long long>(D);
-        const float* de0 = a.det.emb + (fK + ecol[e0]) * static_cast<long long>(D);
-        const float* te1 = a.trk.emb_pool + (sT + t_slot[erow[e1]]) * static_cast<long long>(D);
-        const float* de1 = a.det.emb + (fK + ecol[e1]) * static_cast<long long>(D);
-        double acc0 = 0.0, acc1 = 0.0;
-        if ((D & 3) == 0) {
-          const float4 *t40 = reinterpret_cast<const float4*>(te0), *d40 = reinterpret_cast<const float4*>(de0);
-          const float4 *t41 = reinterpret_cast<const float4*>(te1), *d41 = reinterpret_cast<const float4*>(de1);
-          for (int i = lane; i < D / 4; i += 32) {
-            const float4 x0 = t40[i], y0 = d40[i], x1 = t41[i], y1 = d41[i];
-            acc0 = fma(static_cast<double>(x0.x), static_cast<double>(y0.x), acc0);
-            acc1 = fma(static_cast<double>(x1.x), static_cast<double>(y1.x), acc1);
-            acc0 = fma(static_cast<double>(x0.y), static_cast<double>(y0.y), acc0);
-            acc1 = fma(static_cast<double>(x1.y), static_cast<double>(y1.y), acc1);
-            acc0 = fma(static_cast<double>(x0.z), static_cast<double>(y0.z), acc0);
-            acc1 = fma(static_cast<double>(x1.z), static_cast<double>(y1.z), acc1);
-            acc0 = fma(static_cast<double>(x0.w), static_cast<double>(y0.w), acc0);
-            acc1 = fma(static_cast<double>(x1.w), static_cast<double>(y1.w), acc1);
-          }
-        } else {
-          for (int i = lane; i < D; i += 32) {
-            acc0 = fma(static_cast<double>(te0[i]), static_cast<double>(de0[i]), acc0);
-            acc1 = fma(static_cast<double>(te1[i]), static_cast<double>(de1[i]), acc1);
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          acc0 += __shfl_xor_sync(FULL, acc0, o);
-          acc1 += __shfl_xor_sync(FULL, acc1, o);
-        }
-        const double c0 = fmin(fmax(1.0 - acc0, 0.0), 2.0);
-        const double c1 = fmin(fmax(1.0 - acc1, 0.0), 2.0);
-        if (lane == 0) {
-          eval[e0] = c0;
-          if (two) eval[e1] = c1;
-        }
-        amp = fmax(amp, fabs(c0));
-        if (two) amp = fmax(amp, fabs(c1));
-      }
-      if (lane == 0 && E > 0) {
-        // amplitude = max |finite| (tf/assoc.py:71); non-negative, so an
-        // integer max over the bit patterns is exact.
-        atomicMax(reinterpret_cast<unsigned long long*>(&s_amp), static_cast<unsigned long long>(__double_as_longlong(amp)));
-      }
+      if (tid == 0) s_Efr = E;
     }
     __syncthreads();
-    TF_MARK(3);
-    if (s_err != STATUS_CLEAR) {
-      if (tid == 0) s_status = (b << 8) | (s_err & 0xff);
-      break;
+    // ---- fp64 cosine cost of un-gated pairs (tf/assoc.py:34-46), cluster-wide --
+    if (C > 1) cg::this_cluster().sync();                          // S1: entries ready
+    if (gating) {
+      CostView cv;
+      cv.rowptr = rowptr;
+      cv.ecol = ecol;
+      cv.erow = erow;
+      cv.eval = eval;
+      cv.t_slot = t_slot;
+      cv.work = &s_work;
+      cv.amp = reinterpret_cast<unsigned long long*>(&s_amp);
+      cv.pool = a.trk.emb_pool + sT * static_cast<long long>(D);
+      cv.dets = a.det.emb + fK * static_cast<long long>(D);
+      cv.T = T;
+      cv.E = s_Efr;
+      cv.D = D;
+      cost_work(cv, wid, nw * C);
     }
+    __syncthreads();
+    if (C > 1) cg::this_cluster().sync();                          // S2: costs written
+    if (tid == 0) s_work = 0;
+    TF_MARK(3);
+    // errors from here on finish the frame's cluster barriers, then stop
+    const bool frame_ok = (s_err == STATUS_CLEAR);
+    if (frame_ok) {
 
     // ---- exact LAP (tf/assoc.py:60-87) --------------------------------------
     // The reference pads the gated matrix with a sentinel and solves it with
@@ -1067,67 +1211,31 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       }
       t_flag[t] = remove;
     }
-    // EMA appearance update, one warp per matched detection (tf/tracker.py:67-71,
-    // 117-119): normalize(alpha * old + (1 - alpha) * new) in fp64, fp32 out.
-    for (int k = wid; k < K; k += nw) {
-      const int t = d_row[k];
-      if (t < 0) continue;
-      float* te = a.trk.emb_pool + (sT + t_slot[t]) * static_cast<long long>(D);
-      const float* de = a.det.emb + (fK + k) * static_cast<long long>(D);
-      if (D == 512) {                                   // one pass, rows held in registers
-        const float4* t4 = reinterpret_cast<const float4*>(te);
-        const float4* d4 = reinterpret_cast<const float4*>(de);
-        float4 x[4], y[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) { x[q] = t4[lane + 32 * q]; y[q] = d4[lane + 32 * q]; }
-        double v[16];
-        double ss = 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          v[4 * q + 0] = P.alpha * static_cast<double>(x[q].x) + P.beta * static_cast<double>(y[q].x);
-          v[4 * q + 1] = P.alpha * static_cast<double>(x[q].y) + P.beta * static_cast<double>(y[q].y);
-          v[4 * q + 2] = P.alpha * static_cast<double>(x[q].z) + P.beta * static_cast<double>(y[q].z);
-          v[4 * q + 3] = P.alpha * static_cast<double>(x[q].w) + P.beta * static_cast<double>(y[q].w);
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) ss = fma(v[q], v[q], ss);
-        ss = warp_sum(ss);
-        const double nrm = sqrt(ss);
-        if (!(nrm >= 1e-12) || !isfinite(nrm)) {
-          if (lane == 0) flag_error(&s_err, t + 1, TF_DEGENERATE_EMBEDDING);
-          continue;
-        }
-        float4* o4 = reinterpret_cast<float4*>(te);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float4 r;
-          r.x = static_cast<float>(v[4 * q + 0] / nrm);
-          r.y = static_cast<float>(v[4 * q + 1] / nrm);
-          r.z = static_cast<float>(v[4 * q + 2] / nrm);
-          r.w = static_cast<float>(v[4 * q + 3] / nrm);
-          o4[lane + 32 * q] = r;
-        }
-        continue;
-      }
-      double ss = 0.0;
-      for (int i = lane; i < D; i += 32) {
-        double v = P.alpha * static_cast<double>(te[i]) + P.beta * static_cast<double>(de[i]);
-        ss = fma(v, v, ss);
-      }
-      ss = warp_sum(ss);
-      double nrm = sqrt(ss);
-      if (!(nrm >= 1e-12) || !isfinite(nrm)) {
-        if (lane == 0) flag_error(&s_err, t + 1, TF_DEGENERATE_EMBEDDING);
-        continue;
-      }
-      __syncwarp();
-      for (int i = lane; i < D; i += 32) {
-        double v = P.alpha * static_cast<double>(te[i]) + P.beta * static_cast<double>(de[i]);
-        te[i] = static_cast<float>(v / nrm);
-      }
+    }  // frame_ok
+    if (tid == 0) s_emaK = frame_ok ? K : 0;
+    __syncthreads();
+    if (C > 1) cg::this_cluster().sync();                          // S3: matches ready
+    if (frame_ok) {
+      EmaView ev;
+      ev.d_row = d_row;
+      ev.t_slot = t_slot;
+      ev.work = &s_work;
+      ev.err = &s_err;
+      ev.pool = a.trk.emb_pool + sT * static_cast<long long>(D);
+      ev.dets = a.det.emb + fK * static_cast<long long>(D);
+      ev.alpha = P.alpha;
+      ev.beta = P.beta;
+      ev.K = K;
+      ev.D = D;
+      ema_work(ev);
     }
     __syncthreads();
+    if (C > 1) cg::this_cluster().sync();                          // S4: EMA done
     TF_MARK(6);
+    if (!frame_ok) {                          // errors before the LAP: stop here
+      if (tid == 0) s_status = (b << 8) | (s_err & 0xff);
+      break;
+    }
 
     // ---- records: matched tracks in list (= id) order, then births ---------
     // Births are unmatched detections in ascending order (tf/tracker.py:145-157).
@@ -1257,6 +1365,13 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     }
   }
   __syncthreads();
+  // ---- release the follower CTAs (they wait at the S1 barrier) ----------------
+  if (C > 1) {
+    if (tid == 0) s_cmd = 1;
+    __syncthreads();
+    cg::this_cluster().sync();        // S1': followers read the stop command
+    cg::this_cluster().sync();        // followers are done with this CTA's memory
+  }
   // ---- write the stream's state back -----------------------------------------
   T = s_T;
   for (int t = tid; t < T; t += blockDim.x) {
@@ -1741,8 +1856,58 @@ cudaError_t launch_frame_dets(const double* boxes, const double* obj, const floa
 cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st) {
   const size_t smem = assoc_smem_bytes(a.cap_tracks, a.cap_det, a.cap_entries);
   cudaFuncSetAttribute(associate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  associate_kernel<<<n_streams, kAssocThreads, smem, st>>>(a, P);
-  return cudaGetLastError();
+  if (a.cluster <= 1) {
+    associate_kernel<<<n_streams, kAssocThreads, smem, st>>>(a, P);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(n_streams * a.cluster));
+  cfg.blockDim = dim3(kAssocThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(a.cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, associate_kernel, a, P);
+}
+
+int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entries) {
+  // One stream per cluster; followers only help in the parallel phases, so
+  // spread few streams over up to 8 SMs each, never beyond the SM count.
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const char* env = getenv("TF_CLUSTER");
+  int c = 8;
+  if (env) c = atoi(env);
+  while (c > 1 && n_streams * c > sms) c >>= 1;
+  if (c > 1) {
+    const size_t smem = assoc_smem_bytes(cap_tracks, cap_det, cap_entries);
+    cudaFuncSetAttribute(associate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(c));
+    cfg.blockDim = dim3(kAssocThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(c);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    while (c > 1 && (cudaOccupancyMaxActiveClusters(&clusters, associate_kernel, &cfg) != cudaSuccess || clusters < 1)) {
+      c >>= 1;
+      cfg.gridDim = dim3(static_cast<unsigned>(c));
+      attr[0].val.clusterDim.x = static_cast<unsigned>(c);
+    }
+    cudaGetLastError();
+  }
+  return c < 1 ? 1 : c;
 }
 
 cudaError_t launch_nms_sets(int n_sets, const int* offsets, const double* boxes, const double* scores,

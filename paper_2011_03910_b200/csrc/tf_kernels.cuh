@@ -66,7 +66,8 @@ struct AssocArgs {
   int16_t* pool_col;             // [streams][cap_tracks * cap_det] overflow CSR
   int16_t* pool_row;
   double* pool_val;
-  long long* stats;              // [16] phase cycles / counters (nullptr = off)
+  long long* stats;              // [32] phase cycles / counters (nullptr = off)
+  int cluster;                   // CTAs per stream (1 = no cluster)
 };
 
 struct HeadLaunch {
@@ -86,6 +87,7 @@ cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_
 cudaError_t launch_frame_dets(const double* boxes, const double* obj, const float* emb, const uint8_t* has, int n,
                               int cap_cand, int cap_det, const DetBuf& det, const Params& P, cudaStream_t st);
 cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st);
+int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entries);
 cudaError_t launch_nms_sets(int n_sets, const int* offsets, const double* boxes, const double* scores,
                             const double* thr, uint8_t* keep, int* status, int cap, cudaStream_t st);
 cudaError_t launch_lap_dense(int n, const int* shapes, const long long* cost_off, const double* costs,

@@ -158,3 +158,28 @@ def test_full_size_cfg4_step_properties():
             m = blk.max() if blk.size else 0
             assert m >= last_max[s]
             last_max[s] = m
+
+
+def test_cluster_and_single_cta_association_agree(monkeypatch):
+    """The cluster-cooperative association (followers compute costs / EMA via
+    DSMEM) and the single-CTA path produce identical records and traces."""
+    p, synth = _pkg()
+    outs = []
+    for cl in ("1", "8"):
+        monkeypatch.setenv("TF_CLUSTER", cl)
+        gen = synth.make("cfg1", device="cuda", seed=11)
+        bt = p.BatchTracker(1, frames_per_update=16)
+        res = []
+        for _ in range(3):
+            r = bt.update(gen.next_batch(16), trace=True)
+            tr = bt.trace(16)
+            res.append((r.count.cpu().numpy().copy(), r.track_id.cpu().numpy().copy(), r.box.cpu().numpy().copy(),
+                        tr["det_cost"].cpu().numpy().copy()))
+        outs.append(res)
+    for (c1, i1, b1, k1), (c8, i8, b8, k8) in zip(*outs):
+        assert np.array_equal(c1, c8)
+        for f in range(16):
+            n = c1[f]
+            assert np.array_equal(i1[f, :n], i8[f, :n])
+            assert np.array_equal(b1[f, :n], b8[f, :n])
+            assert np.array_equal(np.nan_to_num(k1[f, :n]), np.nan_to_num(k8[f, :n]))
