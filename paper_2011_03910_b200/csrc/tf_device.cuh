@@ -341,8 +341,27 @@ struct ComponentRows {
   __device__ __forceinline__ double val(int e) const { return eval[e]; }
 };
 
+// Finite entries of local row i = one column of a connected component, when
+// the component is solved transposed (columns as rows): led lists edge ids
+// grouped by local row, rowmap maps a track row to its local column.
+struct TransposedRows {
+  const int* lrp;
+  const int16_t* led;
+  const int16_t* erow;
+  const double* eval;
+  const int16_t* rowmap;
+  __device__ __forceinline__ int begin(int r) const { return lrp[r]; }
+  __device__ __forceinline__ int end(int r) const { return lrp[r + 1]; }
+  __device__ __forceinline__ int col(int q) const { return rowmap[erow[led[q]]]; }
+  __device__ __forceinline__ double val(int q) const { return eval[led[q]]; }
+};
+
+// n_proc: rows processed. The exact reference order needs n_proc == n; when
+// the optimum is known to be unique the padding rows (>= nr) may be skipped,
+// since they only ever take sentinel cells.
 template <class Rows>
-__device__ inline void warp_lap(int n, int nr, const Rows R, double sentinel, LapScratch s) {
+__device__ inline void warp_lap(int n, int nr, const Rows R, double sentinel, LapScratch s, int n_proc = -1) {
+  if (n_proc < 0) n_proc = n;
   const int lane = lane_id();
   for (int j = lane; j < n; j += 32) {
     s.u[j] = 0.0;
@@ -352,7 +371,7 @@ __device__ inline void warp_lap(int n, int nr, const Rows R, double sentinel, La
     s.crow[j] = sentinel;
   }
   __syncwarp();
-  for (int cur = 0; cur < n; ++cur) {
+  for (int cur = 0; cur < n_proc; ++cur) {
     for (int p = lane; p < n; p += 32) s.rem[p] = static_cast<int16_t>(n - 1 - p);
     int live = n, row = cur, nvr = 0, nvc = 0, sink = -1;
     double min_val = 0.0;

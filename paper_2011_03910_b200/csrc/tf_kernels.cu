@@ -411,7 +411,7 @@ struct AssocPlan {
       off_slot, off_mdet, off_rowptr, off_flag, off_npos, off_rpos, off_dm, off_dobj, off_drow, off_dpos, off_gmask,
       off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
       off_vr, off_vc, off_lab, off_cnr, off_cnc, off_cne, off_croot, off_coff, off_cpos, off_crows, off_ccols,
-      off_cmap, off_rcol, off_il, off_epos, off_elist, off_pcmin, off_prmin, off_pccnt, off_pcdeg, off_pcrow, off_prdeg, off_prcnt, off_prc1,
+      off_cmap, off_rcol, off_rmap, off_lrp, off_eoff, off_il, off_epos, off_elist, off_pcmin, off_prmin, off_pccnt, off_pcdeg, off_pcrow, off_prdeg, off_prcnt, off_prc1,
       off_pra, off_pca, off_pkr, off_pkc, total;
 };
 
@@ -469,6 +469,9 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_ccols, 2 * NN)
   TF_TAKE(off_cmap, 2 * K)
   TF_TAKE(off_rcol, 2 * T)
+  TF_TAKE(off_rmap, 2 * T)
+  TF_TAKE(off_lrp, 4 * (2 * NN + 1))
+  TF_TAKE(off_eoff, 4 * (NN + 1))
   TF_TAKE(off_epos, 2 * E)
   TF_TAKE(off_elist, 2 * E)
   // forced-pair peeling
@@ -706,6 +709,9 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   int16_t* c_map = reinterpret_cast<int16_t*>(smem + pl.off_cmap);
   int16_t* rcol = reinterpret_cast<int16_t*>(smem + pl.off_rcol);
   int16_t* c_epos = reinterpret_cast<int16_t*>(smem + pl.off_epos);
+  int16_t* c_rmap = reinterpret_cast<int16_t*>(smem + pl.off_rmap);
+  int* c_lrp = reinterpret_cast<int*>(smem + pl.off_lrp);
+  int* c_eoff = reinterpret_cast<int*>(smem + pl.off_eoff);
   int16_t* c_elist = reinterpret_cast<int16_t*>(smem + pl.off_elist);
   unsigned long long* p_cmin = reinterpret_cast<unsigned long long*>(smem + pl.off_pcmin);
   double* p_rmin = reinterpret_cast<double*>(smem + pl.off_prmin);
@@ -863,28 +869,50 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
 
     // ---- gate (tf/tracker.py:109-110, tf/motion.py:128-142) ----------------
     if (gating) {
-      // one warp per (track, 32-detection chunk): balanced over the CTA
+      // lanes own detections (measurement in registers); each warp walks its
+      // tracks four at a time so four independent fp64 chains are in flight
       const int KC = (K + 31) >> 5;
-      for (int it = wid; it < T * KC; it += nw) {
-        const int t = it / KC, k0 = (it - t * KC) << 5;
-        const int k = k0 + lane;
-        const double* m = &t_mean[8 * t];
-        bool fin = false;
+      for (int kc = 0; kc < KC; ++kc) {
+        const int k = (kc << 5) + lane;
+        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
         if (k < K) {
-          const double* z = &d_meas[4 * k];
-          double g;
-          if (P.gate_metric == 0) {
-            g = KF::mahalanobis(m, &g_il[4 * t], z);
-          } else {
-            double dx = m[0] - z[0], dy = m[1] - z[1];
-            g = dx * dx + dy * dy;
-          }
-          fin = !(g > P.gate_threshold);
+          z0 = d_meas[4 * k];
+          z1 = d_meas[4 * k + 1];
+          z2 = d_meas[4 * k + 2];
+          z3 = d_meas[4 * k + 3];
         }
-        const unsigned bm = __ballot_sync(FULL, fin);
-        if (lane == 0) {
-          gmask[t * KW + (k0 >> 5)] = bm;
-          if (bm) atomicAdd(&t_flag[t], __popc(bm));
+        for (int t0 = 4 * wid; t0 < T; t0 += 4 * nw) {
+          bool fin[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u;
+            fin[u] = false;
+            if (t < T && k < K) {
+              const double* m = &t_mean[8 * t];
+              double g;
+              if (P.gate_metric == 0) {
+                const double* il = &g_il[4 * t];
+                const double x0 = (z0 - m[0]) * il[0];
+                const double x1 = (z1 - m[1]) * il[1];
+                const double x2 = (z2 - m[2]) * il[2];
+                const double x3 = (z3 - m[3]) * il[3];
+                g = ((x0 * x0 + x1 * x1) + x2 * x2) + x3 * x3;
+              } else {
+                const double dx = m[0] - z0, dy = m[1] - z1;
+                g = dx * dx + dy * dy;
+              }
+              fin[u] = !(g > P.gate_threshold);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u;
+            const unsigned bm = __ballot_sync(FULL, fin[u]);
+            if (lane == 0 && t < T) {
+              gmask[t * KW + kc] = bm;
+              if (bm) atomicAdd(&t_flag[t], __popc(bm));
+            }
+          }
         }
       }
     }
@@ -1124,6 +1152,19 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
             if (i < n_multi) c_off[i] = carry + incl - v;
             carry += __shfl_sync(FULL, incl, 31);
           }
+          int ecarry = 0;
+          for (int i0 = 0; i0 < n_multi; i0 += 32) {
+            const int i = i0 + lane;
+            const int v = i < n_multi ? c_ne[c_root[i]] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              int q = __shfl_up_sync(FULL, incl, o);
+              if (lane >= o) incl += q;
+            }
+            if (i < n_multi) c_eoff[i] = ecarry + incl - v;
+            ecarry += __shfl_sync(FULL, incl, 31);
+          }
         }
         __syncthreads();
         for (int i = wid; i < n_multi; i += nw) {
@@ -1133,7 +1174,11 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
             const int t = t0 + lane;
             const bool in = t < T && c_lab[t] == root && p_ra[t];
             const unsigned bm = __ballot_sync(FULL, in);
-            if (in) c_rows[off + nr_l + __popc(bm & ((1u << lane) - 1u))] = static_cast<int16_t>(t);
+            if (in) {
+              const int j = nr_l + __popc(bm & ((1u << lane) - 1u));
+              c_rows[off + j] = static_cast<int16_t>(t);
+              c_rmap[t] = static_cast<int16_t>(j);
+            }
             nr_l += __popc(bm);
           }
           for (int k0 = 0; k0 < K; k0 += 32) {
@@ -1154,14 +1199,53 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
           Ls.path = L.path + off; Ls.row4col = L.row4col + off; Ls.col4row = L.col4row + off;
           Ls.rem = L.rem + off; Ls.vrows = L.vrows + off + i; Ls.vcols = L.vcols + off + i;
           const double sentinel = 2.0 * static_cast<double>(n_l) * fmax(s_amp, 1.0) + 1.0;
-          warp_lap(n_l, nr_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, Ls);
-          __syncwarp();
-          for (int r = lane; r < nr_l; r += 32) {
-            const int j = Ls.col4row[r];
-            if (j < nc_l) {
-              const int t = c_rows[off + r], c = c_cols[off + j];
-              for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
-                if (ecol[e] == c) { rcol[t] = static_cast<int16_t>(c); break; }
+          // The optimum is unique here, so the component is solved from its
+          // smaller side (typically 1-3 detections wanted by many lost tracks)
+          // and the padding rows are skipped.
+          if (nc_l < nr_l) {
+            int* lrp = c_lrp + off + i;                 // nc_l + 1 row pointers
+            int16_t* led = c_epos + c_eoff[i];          // the component's edge ids by detection
+            // counting sort of the component's live edges by detection (lane-parallel)
+            for (int j = lane; j <= nc_l; j += 32) lrp[j] = 0;
+            __syncwarp();
+            for (int q = lane; q < E_live; q += 32) {
+              const int e = c_elist[q];
+              if (c_lab[erow[e]] == root) atomicAdd(&lrp[c_map[ecol[e]] + 1], 1);
+            }
+            __syncwarp();
+            if (lane == 0)
+              for (int j = 0; j < nc_l; ++j) lrp[j + 1] += lrp[j];
+            __syncwarp();
+            for (int q = lane; q < E_live; q += 32) {
+              const int e = c_elist[q];
+              if (c_lab[erow[e]] == root) led[atomicAdd(&lrp[c_map[ecol[e]]], 1)] = static_cast<int16_t>(e);
+            }
+            __syncwarp();
+            if (lane == 0) {                          // cursors advanced to the row ends: shift back
+              for (int j = nc_l; j > 0; --j) lrp[j] = lrp[j - 1];
+              lrp[0] = 0;
+            }
+            __syncwarp();
+            warp_lap(n_l, nc_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, Ls, nc_l);
+            __syncwarp();
+            for (int j = lane; j < nc_l; j += 32) {
+              const int lc = Ls.col4row[j];
+              if (lc < nr_l) {
+                const int t = c_rows[off + lc], c = c_cols[off + j];
+                for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
+                  if (ecol[e] == c) { rcol[t] = static_cast<int16_t>(c); break; }
+              }
+            }
+          } else {
+            warp_lap(n_l, nr_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, Ls, nr_l);
+            __syncwarp();
+            for (int r = lane; r < nr_l; r += 32) {
+              const int j = Ls.col4row[r];
+              if (j < nc_l) {
+                const int t = c_rows[off + r], c = c_cols[off + j];
+                for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
+                  if (ecol[e] == c) { rcol[t] = static_cast<int16_t>(c); break; }
+              }
             }
           }
         }
