@@ -56,7 +56,7 @@ D = 512
 CAPS = {
     "cfg0": dict(max_candidates=512, max_detections=256, max_tracks=256),
     "cfg1": dict(max_candidates=512, max_detections=256, max_tracks=256),
-    "cfg2": dict(max_candidates=1024, max_detections=256, max_tracks=512),
+    "cfg2": dict(max_candidates=768, max_detections=224, max_tracks=384),
     "cfg3": dict(max_candidates=256, max_detections=160, max_tracks=256),
     "cfg4": dict(max_candidates=192, max_detections=96, max_tracks=160),
 }

@@ -34,6 +34,7 @@ struct tf_ctx {
   int16_t* pool_col;
   int16_t* pool_row;
   double* pool_val;
+  int16_t* pool_aux;
   // host mirror of each stream's last stepped frame (ordering checks)
   std::vector<long long> last_frame;
   std::vector<long long> frame_scratch;
@@ -248,9 +249,10 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   // shared-memory budget for the association CTA decides how many CSR entries stay on chip
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  int entries = 2048;
+  // keep as many gated entries on chip as the budget allows (the rest spill to a global pool)
+  int entries = 8192;
   while (entries > 64 && assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + 2048 > static_cast<size_t>(smem_optin))
-    entries /= 2;
+    entries -= 128;
   if (assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + 2048 > static_cast<size_t>(smem_optin) ||
       frame_smem_bytes(54264, k.max_candidates) + 2048 > static_cast<size_t>(smem_optin)) {
     delete c;
@@ -287,6 +289,7 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   A(&c->pool_col, S * Tm * Km);
   A(&c->pool_row, S * Tm * Km);
   A(&c->pool_val, S * Tm * Km);
+  A(&c->pool_aux, 2 * S * Tm * Km);
   A(&c->d_stats, 32);
   if (e != cudaSuccess) {
     std::string m = cudaGetErrorString(e);
@@ -445,6 +448,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
+  a.pool_aux = c->pool_aux;
   a.stats = c->profiling ? c->d_stats : nullptr;
   {
     const char* env = getenv("TF_CLUSTER");
@@ -520,6 +524,7 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
+  a.pool_aux = c->pool_aux;
   a.stats = c->profiling ? c->d_stats : nullptr;
   a.cluster = 1;
   a.out.count = out->count;

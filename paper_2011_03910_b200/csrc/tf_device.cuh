@@ -468,4 +468,182 @@ __device__ inline void warp_lap(int n, int nr, const Rows R, double sentinel, La
   }
 }
 
+// Register-resident variant of warp_lap: lane l owns columns l + 32q (q < RC)
+// and keeps their dual, tentative distance, path, owner and position in the
+// candidate list in registers, so a Dijkstra iteration touches shared memory
+// only for the current row's costs. The tie rule is applied order-free: among
+// equal minima a free column with the largest list position wins, otherwise
+// the smallest position (what scipy's sequential scan yields). Results land
+// in s.col4row (row -> column).
+template <int RC, class Rows>
+__device__ inline void warp_lap_reg(int n, int nr, const Rows R, double sentinel, LapScratch s, int n_proc) {
+  const int lane = lane_id();
+  double v[RC], dist[RC];
+  int path[RC], owner[RC], pos[RC];
+#pragma unroll
+  for (int q = 0; q < RC; ++q) {
+    v[q] = 0.0;
+    dist[q] = 0.0;
+    path[q] = -1;
+    owner[q] = -1;
+  }
+  for (int r = lane; r < n; r += 32) {
+    s.u[r] = 0.0;
+    s.col4row[r] = -1;
+    s.crow[r] = sentinel;
+  }
+  __syncwarp();
+  for (int cur = 0; cur < n_proc; ++cur) {
+#pragma unroll
+    for (int q = 0; q < RC; ++q) {
+      const int j = lane + 32 * q;
+      pos[q] = j < n ? n - 1 - j : -1;
+    }
+    int live = n, row = cur, sink = -1, nvr = 0;
+    unsigned vis = 0u;
+    double min_val = 0.0;
+    bool first = true;
+    while (sink < 0) {
+      int e0 = 0, e1 = 0;
+      if (row < nr) {
+        e0 = R.begin(row);
+        e1 = R.end(row);
+        for (int e = e0 + lane; e < e1; e += 32) {
+          const int c = R.col(e);
+          if (c >= 0) s.crow[c] = R.val(e);
+        }
+      }
+      __syncwarp();
+      double crow[RC];
+#pragma unroll
+      for (int q = 0; q < RC; ++q) {
+        const int j = lane + 32 * q;
+        crow[q] = j < n ? s.crow[j] : sentinel;
+      }
+      const double ur = s.u[row];
+      __syncwarp();
+      if (row < nr)
+        for (int e = e0 + lane; e < e1; e += 32) {
+          const int c = R.col(e);
+          if (c >= 0) s.crow[c] = sentinel;
+        }
+      unsigned long long best = ~0ull;
+      int best_p = -1, best_q = 0;
+      bool best_free = false;
+#pragma unroll
+      for (int q = 0; q < RC; ++q) {
+        if (pos[q] < 0) continue;
+        const double r = ((min_val + crow[q]) - ur) - v[q];
+        if (first || r < dist[q]) {
+          dist[q] = r;
+          path[q] = row;
+        }
+        const unsigned long long k = dkey(dist[q]);
+        const bool fr = owner[q] < 0;
+        const int p = pos[q];
+        bool take;
+        if (best_p < 0 || k < best) take = true;
+        else if (k > best) take = false;
+        else take = fr ? (!best_free || p > best_p) : (!best_free && p < best_p);
+        if (take) {
+          best = k;
+          best_p = p;
+          best_q = q;
+          best_free = fr;
+        }
+      }
+      const unsigned hi = static_cast<unsigned>(best >> 32), lo = static_cast<unsigned>(best);
+      const unsigned mh = __reduce_min_sync(FULL, hi);
+      const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+      const bool qual = best_p >= 0 && hi == mh && lo == ml;
+      const unsigned fmask = __ballot_sync(FULL, qual && best_free);
+      int pw;
+      if (fmask)
+        pw = static_cast<int>(__reduce_max_sync(FULL, (qual && best_free) ? static_cast<unsigned>(best_p) : 0u));
+      else
+        pw = static_cast<int>(__reduce_min_sync(FULL, qual ? static_cast<unsigned>(best_p) : 0xffffffffu));
+      const int wlane = __ffs(__ballot_sync(FULL, best_p == pw)) - 1;
+      double my_d = 0.0;
+      int my_o = -1;
+#pragma unroll
+      for (int q = 0; q < RC; ++q)
+        if (q == best_q) {
+          my_d = dist[q];
+          my_o = owner[q];
+        }
+      const int q_w = __shfl_sync(FULL, best_q, wlane);
+      const int j = wlane + 32 * q_w;
+      min_val = __shfl_sync(FULL, my_d, wlane);
+      const int own = __shfl_sync(FULL, my_o, wlane);
+      if (lane == wlane) {
+#pragma unroll
+        for (int q = 0; q < RC; ++q)
+          if (q == q_w) {
+            vis |= 1u << q;
+            pos[q] = -1;
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < RC; ++q)          // the last list entry moves into the freed slot
+        if (pos[q] == live - 1) pos[q] = pw;
+      --live;
+      if (own < 0) {
+        sink = j;
+      } else {
+        if (lane == 0) {
+          s.vrows[nvr] = static_cast<int16_t>(own);
+          s.dist[nvr] = min_val;
+        }
+        ++nvr;
+        row = own;
+      }
+      first = false;
+    }
+    __syncwarp();
+    // dual update (scipy order: u[cur], visited rows, visited columns)
+    if (lane == 0) s.u[cur] = s.u[cur] + min_val;
+    for (int q2 = lane; q2 < nvr; q2 += 32) {
+      const int r = s.vrows[q2];
+      s.u[r] = s.u[r] + (min_val - s.dist[q2]);
+    }
+#pragma unroll
+    for (int q = 0; q < RC; ++q)
+      if ((vis >> q) & 1u) v[q] = v[q] - (min_val - dist[q]);
+    __syncwarp();
+    // augment along the alternating path
+    int jj = sink;
+    while (true) {
+      const int ql = jj >> 5, ll = jj & 31;
+      int pv = 0;
+#pragma unroll
+      for (int q = 0; q < RC; ++q)
+        if (q == ql) pv = path[q];
+      const int i = __shfl_sync(FULL, pv, ll);
+      if (lane == ll) {
+#pragma unroll
+        for (int q = 0; q < RC; ++q)
+          if (q == ql) owner[q] = i;
+      }
+      const int t = s.col4row[i];
+      __syncwarp();
+      if (lane == 0) s.col4row[i] = static_cast<int16_t>(jj);
+      __syncwarp();
+      jj = t;
+      if (i == cur) break;
+    }
+  }
+}
+
+// Exact solver dispatch: register-resident for n <= 256, shared-memory otherwise.
+template <class Rows>
+__device__ inline void warp_lap_fast(int n, int nr, const Rows R, double sentinel, LapScratch s, int n_proc = -1) {
+  if (n_proc < 0) n_proc = n;
+  if (n <= 32) warp_lap_reg<1>(n, nr, R, sentinel, s, n_proc);
+  else if (n <= 64) warp_lap_reg<2>(n, nr, R, sentinel, s, n_proc);
+  else if (n <= 128) warp_lap_reg<4>(n, nr, R, sentinel, s, n_proc);
+  else if (n <= 256) warp_lap_reg<8>(n, nr, R, sentinel, s, n_proc);
+  else warp_lap(n, nr, R, sentinel, s, n_proc);
+}
+
 }  // namespace tfd
+

@@ -453,8 +453,11 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_rem, 2 * NN)
   TF_TAKE(off_vr, 2 * (2 * NN + 1))
   TF_TAKE(off_vc, 2 * (2 * NN + 1))
-  // connected components / peeling; the gate bitmask (dead once the CSR is
-  // built) shares this region
+  // peeling kill flags persist (zero) across frames: outside the shared region
+  TF_TAKE(off_pkr, T)
+  TF_TAKE(off_pkc, K)
+  // connected components / peeling; the gate bitmask and the gate factors
+  // (dead once the CSR is built) share this region
   const size_t ustart = o;
   p.off_gmask = ustart;
   p.off_il = align16(ustart + 4 * T * KW);
@@ -485,8 +488,6 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_prc1, 4 * T)
   TF_TAKE(off_pra, T)
   TF_TAKE(off_pca, K)
-  TF_TAKE(off_pkr, T)
-  TF_TAKE(off_pkc, K)
   if (o < align16(p.off_il + 32 * T)) o = align16(p.off_il + 32 * T);
 #undef TF_TAKE
   p.total = o;
@@ -708,11 +709,13 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   int16_t* c_cols = reinterpret_cast<int16_t*>(smem + pl.off_ccols);
   int16_t* c_map = reinterpret_cast<int16_t*>(smem + pl.off_cmap);
   int16_t* rcol = reinterpret_cast<int16_t*>(smem + pl.off_rcol);
-  int16_t* c_epos = reinterpret_cast<int16_t*>(smem + pl.off_epos);
+  int16_t* const smem_epos = reinterpret_cast<int16_t*>(smem + pl.off_epos);
+  int16_t* c_epos = smem_epos;
   int16_t* c_rmap = reinterpret_cast<int16_t*>(smem + pl.off_rmap);
   int* c_lrp = reinterpret_cast<int*>(smem + pl.off_lrp);
   int* c_eoff = reinterpret_cast<int*>(smem + pl.off_eoff);
-  int16_t* c_elist = reinterpret_cast<int16_t*>(smem + pl.off_elist);
+  int16_t* const smem_elist = reinterpret_cast<int16_t*>(smem + pl.off_elist);
+  int16_t* c_elist = smem_elist;
   unsigned long long* p_cmin = reinterpret_cast<unsigned long long*>(smem + pl.off_pcmin);
   double* p_rmin = reinterpret_cast<double*>(smem + pl.off_prmin);
   int* p_ccnt = reinterpret_cast<int*>(smem + pl.off_pccnt);
@@ -753,9 +756,12 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   __shared__ double s_amp;
 
   // Large-E overflow: entries go to this stream's global pool.
-  int16_t* ecol = reinterpret_cast<int16_t*>(smem + pl.off_ecol);
-  int16_t* erow = reinterpret_cast<int16_t*>(smem + pl.off_erow);
-  double* eval = reinterpret_cast<double*>(smem + pl.off_eval);
+  int16_t* const smem_ecol = reinterpret_cast<int16_t*>(smem + pl.off_ecol);
+  int16_t* const smem_erow = reinterpret_cast<int16_t*>(smem + pl.off_erow);
+  double* const smem_eval = reinterpret_cast<double*>(smem + pl.off_eval);
+  int16_t* ecol = smem_ecol;
+  int16_t* erow = smem_erow;
+  double* eval = smem_eval;
 
   if (rank != 0) {
     // ---- follower CTA: joins the cost and EMA phases of every frame -------
@@ -777,9 +783,9 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         CostView cv;
         const bool pooled = E > a.cap_entries;
         cv.rowptr = cl.map_shared_rank(rowptr, 0);
-        cv.ecol = pooled ? a.pool_col + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(ecol, 0);
-        cv.erow = pooled ? a.pool_row + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(erow, 0);
-        cv.eval = pooled ? a.pool_val + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(eval, 0);
+        cv.ecol = pooled ? a.pool_col + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(smem_ecol, 0);
+        cv.erow = pooled ? a.pool_row + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(smem_erow, 0);
+        cv.eval = pooled ? a.pool_val + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(smem_eval, 0);
         cv.t_slot = cl.map_shared_rank(t_slot, 0);
         cv.work = cl.map_shared_rank(&s_work, 0);
         cv.amp = reinterpret_cast<unsigned long long*>(cl.map_shared_rank(&s_amp, 0));
@@ -937,11 +943,14 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       }
       __syncthreads();
       const int E = s_E;
-      if (E > a.cap_entries) {
-        ecol = a.pool_col + static_cast<long long>(s) * Tm * Km;
-        erow = a.pool_row + static_cast<long long>(s) * Tm * Km;
-        eval = a.pool_val + static_cast<long long>(s) * Tm * Km;
-      }
+      // entry storage is chosen per frame (follower CTAs make the same choice)
+      const bool pooled = E > a.cap_entries;
+      ecol = pooled ? a.pool_col + static_cast<long long>(s) * Tm * Km : smem_ecol;
+      erow = pooled ? a.pool_row + static_cast<long long>(s) * Tm * Km : smem_erow;
+      eval = pooled ? a.pool_val + static_cast<long long>(s) * Tm * Km : smem_eval;
+      c_epos = pooled ? a.pool_aux + static_cast<long long>(s) * 2 * Tm * Km : smem_epos;
+      c_elist = pooled ? a.pool_aux + static_cast<long long>(s) * 2 * Tm * Km + static_cast<long long>(Tm) * Km
+                       : smem_elist;
       for (int t = wid; t < T; t += nw) {
         int pos = rowptr[t];
         for (int w = 0; w < (K + 31) / 32; ++w) {
@@ -1008,9 +1017,9 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       for (int r = tid; r < T; r += blockDim.x) { rcol[r] = -1; p_ra[r] = 1; }
       for (int c = tid; c < K; c += blockDim.x) { p_ca[c] = 1; c_map[c] = -1; }
       unsigned long long* p_rminb = reinterpret_cast<unsigned long long*>(p_rmin);
-      // entries beyond the on-chip pool (dense gates): solve the padded matrix directly
-      const bool dense = E > a.cap_entries;
-      for (; !dense;) {
+      // edge ids are int16 in the peeling lists: beyond that, solve the padded matrix
+      const bool huge = E > 32767;
+      for (; !huge;) {
         for (int c = tid; c < K; c += blockDim.x) { p_cmin[c] = ~0ull; p_ccnt[c] = 0; p_cdeg[c] = 0; }
         for (int r = tid; r < T; r += blockDim.x) { p_rminb[r] = ~0ull; p_rcnt[r] = 0; p_rdeg[r] = 0; }
         if (tid == 0) s_flag = 0;
@@ -1066,8 +1075,8 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       }
       TF_SUB(17);
       // residual edges, compacted in CSR order
-      const int E_live = dense ? 0 : block_rank(E, [&](int e) { return p_ra[erow[e]] && p_ca[ecol[e]]; }, c_epos, s_warp);
-      if (!dense)
+      const int E_live = huge ? 0 : block_rank(E, [&](int e) { return p_ra[erow[e]] && p_ca[ecol[e]]; }, c_epos, s_warp);
+      if (!huge)
         for (int e = tid; e < E; e += blockDim.x)
           if (c_epos[e] >= 0) c_elist[c_epos[e]] = static_cast<int16_t>(e);
       for (int x = tid; x < NN; x += blockDim.x) {
@@ -1076,7 +1085,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         c_nc[x] = 0;
         c_ne[x] = 0;
       }
-      if (tid == 0) { s_flag = 1; s_tie = dense; }
+      if (tid == 0) { s_flag = 1; s_tie = huge; }
       for (;;) {
         __syncthreads();
         const int go = s_flag;
@@ -1122,7 +1131,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         if (wid == 0) {
           const int n = T > K ? T : K;
           const double sentinel = 2.0 * static_cast<double>(n) * fmax(s_amp, 1.0) + 1.0;
-          warp_lap(n, T, CsrRows{rowptr, ecol, eval}, sentinel, L);
+          warp_lap_fast(n, T, CsrRows{rowptr, ecol, eval}, sentinel, L);
           __syncwarp();
           for (int r = lane; r < T; r += 32) {
             const int c = L.col4row[r];
@@ -1226,7 +1235,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
               lrp[0] = 0;
             }
             __syncwarp();
-            warp_lap(n_l, nc_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, Ls, nc_l);
+            warp_lap_fast(n_l, nc_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, Ls, nc_l);
             __syncwarp();
             for (int j = lane; j < nc_l; j += 32) {
               const int lc = Ls.col4row[j];
@@ -1237,7 +1246,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
               }
             }
           } else {
-            warp_lap(n_l, nr_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, Ls, nr_l);
+            warp_lap_fast(n_l, nr_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, Ls, nr_l);
             __syncwarp();
             for (int r = lane; r < nr_l; r += 32) {
               const int j = Ls.col4row[r];
@@ -1570,7 +1579,7 @@ __global__ void lap_dense_kernel(const int* shapes, const long long* cost_off, c
   L.rem = reinterpret_cast<int16_t*>(smem + o); o += 2 * n;
   L.vrows = reinterpret_cast<int16_t*>(smem + o); o += 2 * (n + 1);
   L.vcols = reinterpret_cast<int16_t*>(smem + o);
-  warp_lap(n, nr, CsrRows{rowptr, ecol, eval}, sentinel, L);
+  warp_lap_fast(n, nr, CsrRows{rowptr, ecol, eval}, sentinel, L);
   __syncwarp();
   for (int r = lane; r < nr; r += 32) {
     int col = L.col4row[r];

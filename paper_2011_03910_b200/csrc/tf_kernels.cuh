@@ -66,6 +66,7 @@ struct AssocArgs {
   int16_t* pool_col;             // [streams][cap_tracks * cap_det] overflow CSR
   int16_t* pool_row;
   double* pool_val;
+  int16_t* pool_aux;             // [streams][2 * cap_tracks * cap_det] overflow edge lists
   long long* stats;              // [32] phase cycles / counters (nullptr = off)
   int cluster;                   // CTAs per stream (1 = no cluster)
 };
