@@ -273,7 +273,8 @@ def run_ours(args):
     batches = None if streamed else [gen.next_batch(B) for _ in range(W + K)]
     torch.cuda.synchronize()
 
-    bt = p.BatchTracker(S, frames_per_update=B, capacity=cap)
+    pipe = not (streamed or args.no_pipeline)
+    bt = p.BatchTracker(S, frames_per_update=B, capacity=cap, pipeline=pipe)
     eng, lib = bt.engine, bt.engine.lib
     stream = torch.cuda.current_stream()
 
@@ -306,6 +307,7 @@ def run_ours(args):
             e_start.record(stream)
             for i in range(W, W + K):
                 bt.update(batches[i], trace=False, sync=False)
+            bt.join()                      # the timed region ends after the last association
             e_end.record(stream)
             e_end.synchronize()
             ms = e_start.elapsed_time(e_end)
@@ -342,13 +344,14 @@ def run_ours(args):
             tuple(h.cpu().pin_memory() for h in batches[i].heads),
             tuple(e.cpu().contiguous(memory_format=torch.channels_last).pin_memory() for e in batches[i].embs))
             for i in range(1 + e2e_steps)]
-        bt2 = p.BatchTracker(S, frames_per_update=B, capacity=cap)
+        bt2 = p.BatchTracker(S, frames_per_update=B, capacity=cap, pipeline=pipe)
         hout = bt2.host_output(F)
         bt2.update(host_batches[0], host_out=hout)            # warm-up (allocates staging)
         barrier()
         e_start.record(stream)
         for i in range(1, 1 + e2e_steps):
             bt2.update(host_batches[i], host_out=hout, sync=False)
+        bt2.join()                         # ... and after the last records reached host memory
         e_end.record(stream)
         e_end.synchronize()
         bt2.engine.finish()
@@ -412,6 +415,7 @@ def run_ours(args):
                        "l2_policy": f"each step reads a fresh {step_bytes / 2**20:.0f} MB batch (> 126 MB L2)",
                        "generation": "streamed between steps, steps timed one by one" if streamed
                        else "pre-generated on device",
+                       "pipeline": "decode of step i+1 overlaps association of step i" if pipe else "off",
                        "parallelism": f"streams sharded over {world} rank(s), final NCCL all_gather"},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps if e2e_ms else 0,
@@ -461,12 +465,13 @@ def main():
     ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--batch", type=int, default=None, help="frames per stream per update (default: config's B)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--e2e-host-gb", type=float, default=24.0)
     ap.add_argument("--cpu-frames", type=int, default=640)
     ap.add_argument("--cpu-stream-frames", type=int, default=40)
     ap.add_argument("--ref-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true", help="serialise decode and association")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

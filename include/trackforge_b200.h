@@ -179,9 +179,19 @@ int tf_step_detections(tf_ctx* ctx, int32_t stream, int64_t frame_index, int32_t
                        const uint8_t* has_embedding, const tf_records* out, const tf_trace* trace,
                        void* cuda_stream);
 
-/* Synchronise `cuda_stream` and collect device-side errors of the preceding
- * update/step calls. Returns the first error (in stream, then frame order). */
+/* Synchronise `cuda_stream` (and the pipeline's side stream) and collect the
+ * device-side errors of all update/step calls since the previous tf_finish.
+ * Returns the first error (in stream, then frame order). */
 int tf_finish(tf_ctx* ctx, void* cuda_stream);
+
+/* Pipelining (the paper's PP stage overlap). When enabled,
+ * tf_update_heads runs the decode of update i (H2D copies + frame kernel) on
+ * the caller's stream and the association + outputs on a context-owned side
+ * stream, with two detection-buffer sets, so the decode of update i+1 overlaps
+ * the association of update i. Outputs of an update are valid after
+ * tf_finish, or on any stream made to wait with tf_join. */
+int tf_set_pipeline(tf_ctx* ctx, int32_t enabled);
+int tf_join(tf_ctx* ctx, void* cuda_stream);
 
 /* Copy one stream's tracks into caller HOST buffers (synchronising). */
 int tf_export_tracks(tf_ctx* ctx, int32_t stream, tf_track_export* out, void* cuda_stream);

@@ -76,6 +76,8 @@ _SIGS = {
                                    C.POINTER(TfRecords), C.POINTER(TfTrace), c_vp]),
     "tf_finish": (c_i32, [c_vp, c_vp]),
     "tf_export_tracks": (c_i32, [c_vp, c_i32, C.POINTER(TfTrackExport), c_vp]),
+    "tf_set_pipeline": (c_i32, [c_vp, c_i32]),
+    "tf_join": (c_i32, [c_vp, c_vp]),
     "tf_set_profiling": (c_i32, [c_vp, c_i32]),
     "tf_kernel_times": (c_i32, [c_vp, C.POINTER(c_dbl), C.POINTER(c_dbl), C.POINTER(c_i64)]),
     "tf_phase_stats": (c_i32, [c_vp, c_vp]),

@@ -6,6 +6,7 @@
 //   frame_heads_kernel  (S*B CTAs)   decode + NMS + gather/normalise
 //   associate_kernel    (S CTAs)     B frames per stream, sequential per stream
 //   [host output only] cudaMemcpyAsync of the records
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -27,8 +28,24 @@ struct tf_ctx {
   std::string err;
   int cap_entries;
   // per-frame detection buffers
-  DetBuf det;
-  long long* d_frame_index;
+  DetBuf det;                 // = dets[0] (per-frame detection buffers)
+  long long* d_frame_index;   // = d_fidx[0]
+  // pipelining (tf_set_pipeline): two buffer sets, decode on the caller's
+  // stream, association + outputs on `side`
+  DetBuf dets[2];
+  long long* d_fidx[2];
+  int pipeline, parity;
+  cudaStream_t side;
+  cudaEvent_t ev_dec[2], ev_asc[2];
+  bool asc_pending[2];
+  int touched_lo, touched_hi;
+  // pinned staging ring for the per-update frame indices (a pageable H2D copy
+  // may block the host and stall the pipeline)
+  static constexpr int kRing = 4;
+  long long* h_fidx[kRing];
+  cudaEvent_t ev_fidx[kRing];
+  bool fidx_used[kRing];
+  int ring;
   // per-stream track tables
   TrackBuf trk;
   int16_t* pool_col;
@@ -39,8 +56,8 @@ struct tf_ctx {
   std::vector<long long> last_frame;
   std::vector<long long> frame_scratch;
   // device staging used when inputs / outputs are host memory
-  float* stage_conf[3];
-  size_t stage_conf_elems[3];
+  float* stage_conf[2][3];
+  size_t stage_conf_elems[2][3];
   int* rec_count;
   long long* rec_id;
   double* rec_box;
@@ -186,17 +203,31 @@ __global__ void copy_codes_kernel(const int* count, const int* code, int* out, i
     out[static_cast<long long>(f) * cap_det + k] = code[static_cast<long long>(f) * cap_det + k];
 }
 
+// Stage host frame indices through the pinned ring and copy them to `dst`.
+cudaError_t upload_frame_index(tf_ctx* c, long long* dst, const long long* src, int n, cudaStream_t st) {
+  const int r = c->ring;
+  c->ring = (c->ring + 1) % tf_ctx::kRing;
+  cudaError_t e = cudaSuccess;
+  if (c->fidx_used[r]) e = cudaEventSynchronize(c->ev_fidx[r]);
+  if (e != cudaSuccess) return e;
+  std::memcpy(c->h_fidx[r], src, sizeof(long long) * n);
+  e = cudaMemcpyAsync(dst, c->h_fidx[r], sizeof(long long) * n, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  c->fidx_used[r] = true;
+  return cudaEventRecord(c->ev_fidx[r], st);
+}
+
 cudaError_t prof_mark(tf_ctx* c, int which, cudaStream_t st) {
   if (!c->profiling) return cudaSuccess;
   const size_t idx = c->events_used + which;
   while (c->events.size() <= idx) {
     cudaEvent_t e;
-    cudaError_t r = cudaEventCreate(&e);
+    cudaError_t r = cudaEventCreate(&e);   // timing events
     if (r != cudaSuccess) return r;
     c->events.push_back(e);
   }
   cudaError_t r = cudaEventRecord(c->events[idx], st);
-  if (which == 2) c->events_used += 3;
+  if (which == 3) c->events_used += 4;
   return r;
 }
 
@@ -236,9 +267,21 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   c->prof_frames = 0;
   c->cluster_key = -1;
   c->cluster_val = 1;
-  for (int i = 0; i < 3; ++i) {
-    c->stage_conf[i] = nullptr;
-    c->stage_conf_elems[i] = 0;
+  for (int b = 0; b < 2; ++b)
+    for (int i = 0; i < 3; ++i) {
+      c->stage_conf[b][i] = nullptr;
+      c->stage_conf_elems[b][i] = 0;
+    }
+  c->pipeline = 0;
+  c->parity = 0;
+  c->side = nullptr;
+  c->asc_pending[0] = c->asc_pending[1] = false;
+  c->touched_lo = 1 << 30;
+  c->touched_hi = -1;
+  c->ring = 0;
+  for (int r = 0; r < tf_ctx::kRing; ++r) {
+    c->h_fidx[r] = nullptr;
+    c->fidx_used[r] = false;
   }
   if (cudaSetDevice(device) != cudaSuccess) {
     delete c;
@@ -263,14 +306,16 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   auto A = [&](auto** p, size_t n) {
     if (e == cudaSuccess) e = dev_alloc(c, p, n);
   };
-  A(&c->det.count, F);
-  A(&c->det.cand_count, F);
-  A(&c->det.status, F);
-  A(&c->det.meas, F * Km * 4);
-  A(&c->det.obj, F * Km);
-  A(&c->det.code, F * Km);
-  A(&c->det.emb, F * Km * D);
-  A(&c->d_frame_index, F);
+  for (int b = 0; b < 2; ++b) {
+    A(&c->dets[b].count, F);
+    A(&c->dets[b].cand_count, F);
+    A(&c->dets[b].status, F);
+    A(&c->dets[b].meas, F * Km * 4);
+    A(&c->dets[b].obj, F * Km);
+    A(&c->dets[b].code, F * Km);
+    A(&c->dets[b].emb, F * Km * D);
+    A(&c->d_fidx[b], F);
+  }
   A(&c->trk.id, S * Tm);
   A(&c->trk.state, S * Tm);
   A(&c->trk.hits, S * Tm);
@@ -296,6 +341,21 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
     tf_destroy(c);
     return TF_CUDA;
   }
+  c->det = c->dets[0];
+  c->d_frame_index = c->d_fidx[0];
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    e = cudaEventCreateWithFlags(&c->ev_dec[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_asc[b], cudaEventDisableTiming);
+  }
+  for (int r = 0; r < tf_ctx::kRing && e == cudaSuccess; ++r) {
+    e = cudaHostAlloc(&c->h_fidx[r], sizeof(long long) * F, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fidx[r], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    tf_destroy(c);
+    return TF_CUDA;
+  }
   c->last_frame.assign(S, std::numeric_limits<long long>::min());
   reset_streams_kernel<<<static_cast<unsigned>(S), 256>>>(c->trk, 0, static_cast<int>(S), k.max_tracks);
   e = cudaDeviceSynchronize();
@@ -311,6 +371,20 @@ int tf_destroy(tf_ctx* ctx) {
   if (!ctx) return TF_OK;
   cudaSetDevice(ctx->device);
   for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(ctx->ev_dec[b]);
+      cudaEventDestroy(ctx->ev_asc[b]);
+    }
+    cudaStreamDestroy(ctx->side);
+  }
+  for (int r = 0; r < tf_ctx::kRing; ++r)
+    if (ctx->h_fidx[r]) {
+      cudaEventSynchronize(ctx->ev_fidx[r]);
+      cudaEventDestroy(ctx->ev_fidx[r]);
+      cudaFreeHost(ctx->h_fidx[r]);
+    }
   for (void* p : ctx->allocs) cudaFree(p);
   delete ctx;
   return TF_OK;
@@ -320,6 +394,8 @@ int tf_reset_stream(tf_ctx* c, int32_t stream, void* cuda_stream) {
   if (!c) return TF_ARGUMENT;
   if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  for (int b = 0; b < 2; ++b)
+    if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
   reset_streams_kernel<<<1, 256, 0, st>>>(c->trk, stream, 1, c->cap.max_tracks);
   TF_CUDA(c, cudaGetLastError());
   c->last_frame[stream] = std::numeric_limits<long long>::min();
@@ -364,14 +440,22 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     if (rc) return rc;
   }
   TF_CUDA(c, cudaSetDevice(c->device));
-  TF_CUDA(c, cudaMemcpyAsync(c->d_frame_index, frame_index, sizeof(long long) * F, cudaMemcpyHostToDevice, st));
+  // buffer set and streams: without pipelining everything runs on `st` with set 0;
+  // with pipelining the decode of this update (on `st`) overlaps the previous
+  // update's association (on the side stream)
+  const int par = c->pipeline ? c->parity : 0;
+  if (c->pipeline) c->parity ^= 1;
+  cudaStream_t ast = c->pipeline ? c->side : st;           // association + outputs
+  if (c->pipeline && c->asc_pending[par]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[par], 0));
+  DetBuf& det = c->dets[par];
+  TF_CUDA(c, upload_frame_index(c, c->d_fidx[par], reinterpret_cast<const long long*>(frame_index), F, st));
 
   HeadLaunch h;
   h.heads = heads;
   h.frames = F;
   h.cap_cand = c->cap.max_candidates;
   h.cap_det = c->cap.max_detections;
-  h.det = c->det;
+  h.det = det;
   tf_heads staged = *heads;
   if (heads->host_memory) {
     // Confidence planes (channels 4,5 of every anchor) go over PCIe with the copy
@@ -381,11 +465,11 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
       const tf_head_scale& s = heads->scale[i];
       const size_t hw = static_cast<size_t>(s.height) * s.width;
       const size_t need = static_cast<size_t>(F) * 24 * hw;
-      if (c->stage_conf_elems[i] < need) {
+      if (c->stage_conf_elems[par][i] < need) {
         float* p = nullptr;
         TF_CUDA(c, dev_alloc(c, &p, need));
-        c->stage_conf[i] = p;
-        c->stage_conf_elems[i] = need;
+        c->stage_conf[par][i] = p;
+        c->stage_conf_elems[par][i] = need;
       }
       // staging keeps the [F][24][H][W] geometry; only conf planes are filled.
       // Rows of the 2D copy are (frame, anchor) pairs of 2 planes each; frames
@@ -395,13 +479,13 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
       const int rows = uniform ? 4 * F : 4;
       for (int f = 0; f < calls; ++f) {
         const float* src = s.head + static_cast<long long>(f) * s.head_stride_n + 4 * s.head_stride_c;
-        float* dst = c->stage_conf[i] + static_cast<size_t>(f) * 24 * hw + 4 * hw;
+        float* dst = c->stage_conf[par][i] + static_cast<size_t>(f) * 24 * hw + 4 * hw;
         TF_CUDA(c, cudaMemcpy2DAsync(dst, 6 * hw * sizeof(float), src, 6 * s.head_stride_c * sizeof(float),
                                      2 * hw * sizeof(float), rows, cudaMemcpyHostToDevice, st));
       }
       staged.scale[i].head_stride_n = static_cast<long long>(24 * hw);
       staged.scale[i].head_stride_c = static_cast<long long>(hw);
-      h.head_ptr[i] = c->stage_conf[i];
+      h.head_ptr[i] = c->stage_conf[par][i];
       void* dptr = nullptr;
       TF_CUDA(c, cudaHostGetDevicePointer(&dptr, const_cast<float*>(s.emb), 0));
       h.emb_ptr[i] = static_cast<const float*>(dptr);
@@ -434,12 +518,16 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   TF_CUDA(c, prof_mark(c, 0, st));
   TF_CUDA(c, launch_frame_heads(h, c->P, st));
   TF_CUDA(c, prof_mark(c, 1, st));
+  if (c->pipeline) {
+    TF_CUDA(c, cudaEventRecord(c->ev_dec[par], st));
+    TF_CUDA(c, cudaStreamWaitEvent(ast, c->ev_dec[par], 0));
+  }
 
   AssocArgs a;
-  a.det = c->det;
+  a.det = det;
   a.trk = c->trk;
   a.trace = to_trace(trace);
-  a.frame_index = c->d_frame_index;
+  a.frame_index = c->d_fidx[par];
   a.stream_begin = stream_begin;
   a.B = B;
   a.cap_tracks = c->cap.max_tracks;
@@ -474,17 +562,24 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     a.out.objectness = out->objectness;
   }
   a.out.max_records = out->max_records;
-  TF_CUDA(c, launch_associate(a, n_streams, c->P, st));
-  TF_CUDA(c, prof_mark(c, 2, st));
+  TF_CUDA(c, prof_mark(c, 2, ast));
+  TF_CUDA(c, launch_associate(a, n_streams, c->P, ast));
+  TF_CUDA(c, prof_mark(c, 3, ast));
+  if (c->pipeline) {
+    TF_CUDA(c, cudaEventRecord(c->ev_asc[par], ast));
+    c->asc_pending[par] = true;
+  }
   if (trace && trace->det_code)
-    copy_codes_kernel<<<F, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, F, c->cap.max_detections);
+    copy_codes_kernel<<<F, 128, 0, ast>>>(det.count, det.code, trace->det_code, F, c->cap.max_detections);
   if (host_out) {
     const size_t n = static_cast<size_t>(F) * out->max_records;
-    TF_CUDA(c, cudaMemcpyAsync(out->count, c->rec_count, sizeof(int) * F, cudaMemcpyDeviceToHost, st));
-    TF_CUDA(c, cudaMemcpyAsync(out->track_id, c->rec_id, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
-    TF_CUDA(c, cudaMemcpyAsync(out->box, c->rec_box, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, st));
-    TF_CUDA(c, cudaMemcpyAsync(out->objectness, c->rec_obj, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    TF_CUDA(c, cudaMemcpyAsync(out->count, c->rec_count, sizeof(int) * F, cudaMemcpyDeviceToHost, ast));
+    TF_CUDA(c, cudaMemcpyAsync(out->track_id, c->rec_id, sizeof(long long) * n, cudaMemcpyDeviceToHost, ast));
+    TF_CUDA(c, cudaMemcpyAsync(out->box, c->rec_box, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, ast));
+    TF_CUDA(c, cudaMemcpyAsync(out->objectness, c->rec_obj, sizeof(double) * n, cudaMemcpyDeviceToHost, ast));
   }
+  c->touched_lo = std::min(c->touched_lo, stream_begin);
+  c->touched_hi = std::max(c->touched_hi, stream_begin + n_streams);
   for (int ls = 0; ls < n_streams; ++ls)
     c->last_frame[stream_begin + ls] = frame_index[static_cast<size_t>(ls) * B + B - 1];
   c->last_begin = stream_begin;
@@ -508,7 +603,9 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   TF_CUDA(c, cudaSetDevice(c->device));
-  TF_CUDA(c, cudaMemcpyAsync(c->d_frame_index, &fi, sizeof(long long), cudaMemcpyHostToDevice, st));
+  for (int b = 0; b < 2; ++b)
+    if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
+  TF_CUDA(c, upload_frame_index(c, c->d_frame_index, &fi, 1, st));
   TF_CUDA(c, launch_frame_dets(boxes, objectness, embeddings, has_embedding, n, c->cap.max_candidates,
                                c->cap.max_detections, c->det, c->P, st));
   AssocArgs a;
@@ -536,8 +633,8 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   if (trace && trace->det_code)
     copy_codes_kernel<<<1, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, 1, c->cap.max_detections);
   c->last_frame[stream] = fi;
-  c->last_begin = stream;
-  c->last_count = 1;
+  c->touched_lo = std::min(c->touched_lo, static_cast<int>(stream));
+  c->touched_hi = std::max(c->touched_hi, static_cast<int>(stream) + 1);
   return TF_OK;
 }
 
@@ -545,17 +642,39 @@ int tf_finish(tf_ctx* c, void* cuda_stream) {
   if (!c) return TF_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   TF_CUDA(c, cudaStreamSynchronize(st));
-  if (c->last_count == 0) return TF_OK;
-  std::vector<int> status(c->last_count);
-  TF_CUDA(c, cudaMemcpy(status.data(), c->trk.status + c->last_begin, sizeof(int) * c->last_count,
-                        cudaMemcpyDeviceToHost));
-  for (int i = 0; i < c->last_count; ++i) {
+  if (c->side) TF_CUDA(c, cudaStreamSynchronize(c->side));
+  c->asc_pending[0] = c->asc_pending[1] = false;
+  if (c->touched_hi <= c->touched_lo) return TF_OK;
+  const int lo = c->touched_lo, n = c->touched_hi - c->touched_lo;
+  c->touched_lo = 1 << 30;
+  c->touched_hi = -1;
+  std::vector<int> status(n);
+  TF_CUDA(c, cudaMemcpy(status.data(), c->trk.status + lo, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemset(c->trk.status + lo, 0, sizeof(int) * n));
+  for (int i = 0; i < n; ++i) {
     if (status[i] != 0) {
       const int code = status[i] & 0xff, frame = status[i] >> 8;
-      return fail(c, code, std::string(tf_status_name(code)) + " in stream " + std::to_string(c->last_begin + i) +
+      return fail(c, code, std::string(tf_status_name(code)) + " in stream " + std::to_string(lo + i) +
                                " at batch frame " + std::to_string(frame));
     }
   }
+  return TF_OK;
+}
+
+int tf_set_pipeline(tf_ctx* c, int32_t enabled) {
+  if (!c) return TF_ARGUMENT;
+  if (c->side) TF_CUDA(c, cudaStreamSynchronize(c->side));
+  c->asc_pending[0] = c->asc_pending[1] = false;
+  c->pipeline = enabled ? 1 : 0;
+  c->parity = 0;
+  return TF_OK;
+}
+
+int tf_join(tf_ctx* c, void* cuda_stream) {
+  if (!c) return TF_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  for (int b = 0; b < 2; ++b)
+    if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
   return TF_OK;
 }
 
@@ -564,6 +683,7 @@ int tf_export_tracks(tf_ctx* c, int32_t stream, tf_track_export* o, void* cuda_s
   if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   TF_CUDA(c, cudaStreamSynchronize(st));
+  if (c->side) TF_CUDA(c, cudaStreamSynchronize(c->side));
   const long long Tm = c->cap.max_tracks, D = c->cfg.embedding_dim;
   const long long base = stream * Tm;
   int n = 0;
@@ -620,13 +740,13 @@ int tf_kernel_times(tf_ctx* c, double* frame_ms, double* assoc_ms, int64_t* upda
   if (!c || !frame_ms || !assoc_ms || !updates) return TF_ARGUMENT;
   *frame_ms = 0.0;
   *assoc_ms = 0.0;
-  *updates = static_cast<int64_t>(c->events_used / 3);
+  *updates = static_cast<int64_t>(c->events_used / 4);
   if (c->events_used == 0) return TF_OK;
   TF_CUDA(c, cudaEventSynchronize(c->events[c->events_used - 1]));
-  for (size_t i = 0; i + 2 < c->events_used; i += 3) {
+  for (size_t i = 0; i + 3 < c->events_used; i += 4) {
     float a = 0.f, b = 0.f;
     TF_CUDA(c, cudaEventElapsedTime(&a, c->events[i], c->events[i + 1]));
-    TF_CUDA(c, cudaEventElapsedTime(&b, c->events[i + 1], c->events[i + 2]));
+    TF_CUDA(c, cudaEventElapsedTime(&b, c->events[i + 2], c->events[i + 3]));
     *frame_ms += a;
     *assoc_ms += b;
   }

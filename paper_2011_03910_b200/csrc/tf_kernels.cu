@@ -1483,7 +1483,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     tb.n_tracks[s] = T;
     tb.next_id[s] = s_next;
     tb.n_free[s] = s_nfree;
-    tb.status[s] = s_status;
+    if (s_status) tb.status[s] = s_status;    // sticky until tf_finish reads it
   }
 }
 

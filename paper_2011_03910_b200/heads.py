@@ -109,7 +109,11 @@ class BatchTracker:
     """S independent trackers updated with B frames each per call."""
 
     def __init__(self, num_streams: int, config: TrackerConfig | None = None, *, frames_per_update: int = 8,
-                 capacity: Capacity | None = None, quantize: bool = False):
+                 capacity: Capacity | None = None, quantize: bool = False, pipeline: bool = False):
+        """``pipeline=True`` overlaps the decode of update i+1 with the
+        association of update i (the paper's PP stage): the
+        association runs on a context-owned CUDA stream; results are valid
+        after ``finish()`` (``update(sync=True)`` calls it) or ``join()``."""
         self.config = config or TrackerConfig()
         self.S = int(num_streams)
         cap = capacity or Capacity(streams=self.S, max_frames=self.S * frames_per_update)
@@ -117,6 +121,17 @@ class BatchTracker:
             raise ValueError("capacity.streams < num_streams")
         self.engine = Engine(self.config, cap, quantize=quantize)
         self.frame = np.full(self.S, -1, np.int64)
+        self.pipeline = bool(pipeline)
+        if self.pipeline:
+            self.engine.check(self.engine.lib.tf_set_pipeline(self.engine.ctx, 1), "pipeline")
+
+    def join(self, stream=None) -> None:
+        """Make ``stream`` (default: current) wait for all queued association work."""
+        self.engine.check(self.engine.lib.tf_join(self.engine.ctx, _lib.stream_handle(stream)), "join")
+
+    def finish(self) -> None:
+        """Synchronise and raise the first device-side error of the queued updates."""
+        self.engine.finish()
 
     def _frames(self, n_streams: int, B: int, frame_index) -> np.ndarray:
         if frame_index is None:

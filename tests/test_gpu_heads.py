@@ -185,3 +185,34 @@ def test_cluster_and_single_cta_association_agree(monkeypatch):
             assert np.array_equal(i1[f, :n], i8[f, :n])
             assert np.array_equal(b1[f, :n], b8[f, :n])
             assert np.array_equal(np.nan_to_num(k1[f, :n]), np.nan_to_num(k8[f, :n]))
+
+
+def test_pipelined_updates_match_serial():
+    """Pipelining (decode of update i+1 overlapping association of update i on
+    a side stream, double-buffered detections) gives the serial results."""
+    p, synth = _pkg()
+    res = []
+    for pipe in (False, True):
+        gen = synth.make("cfg1", device="cuda", seed=5)
+        batches = [gen.next_batch(8) for _ in range(4)]
+        bt = p.BatchTracker(1, frames_per_update=8, pipeline=pipe)
+        hout = [bt.host_output(8) for _ in batches] if pipe else None
+        outs = []
+        for i, bb in enumerate(batches):
+            if pipe:
+                pinned = p.HeadOutputs(tuple(h.cpu().pin_memory() for h in bb.heads),
+                                       tuple(e.cpu().pin_memory() for e in bb.embs))
+                r = bt.update(pinned, host_out=hout[i], sync=False)
+                outs.append(r)                       # distinct pinned buffers per update
+            else:
+                r = bt.update(bb)
+                outs.append((r.count.cpu().numpy().copy(), r.track_id.cpu().numpy().copy()))
+        bt.finish()
+        if pipe:
+            outs = [(o.count.numpy().copy(), o.track_id.numpy().copy()) for o in outs]
+        res.append(outs)
+    for (c0, i0), (c1, i1) in zip(*res):
+        assert np.array_equal(np.asarray(c0), np.asarray(c1))
+        for f in range(8):
+            n = int(c0[f])
+            assert np.array_equal(i0[f, :n], i1[f, :n])
