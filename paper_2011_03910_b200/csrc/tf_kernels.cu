@@ -412,7 +412,7 @@ struct AssocPlan {
       off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
       off_vr, off_vc, off_lab, off_cnr, off_cnc, off_cne, off_croot, off_coff, off_cpos, off_crows, off_ccols,
       off_cmap, off_rcol, off_rmap, off_lrp, off_eoff, off_il, off_epos, off_elist, off_pcmin, off_prmin, off_pccnt, off_pcdeg, off_pcrow, off_prdeg, off_prcnt, off_prc1,
-      off_pra, off_pca, off_pkr, off_pkc, total;
+      off_pra, off_pca, off_pkr, off_pkc, off_emas, total;
 };
 
 __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
@@ -439,6 +439,7 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_dobj, 8 * K)
   TF_TAKE(off_drow, 4 * K)
   TF_TAKE(off_dpos, 2 * K)
+  TF_TAKE(off_emas, 4 * K)        // EMA work list of the frame (det -> pool slot), read by followers
   TF_TAKE(off_ecol, 2 * E)
   TF_TAKE(off_erow, 2 * E)
   TF_TAKE(off_eval, 8 * E)
@@ -580,8 +581,7 @@ __device__ void cost_work(const CostView v, int worker, int n_workers) {
 }
 
 struct EmaView {
-  const int* d_row;            // matched track row of each detection, -1 if none
-  const int* t_slot;
+  const int* slot;             // pool slot of each detection's matched track, -1 if none
   int* work;
   int* err;
   float* pool;
@@ -599,9 +599,9 @@ __device__ void ema_work(const EmaView v) {
     if (lane == 0) k = atomicAdd(v.work, 1);
     k = __shfl_sync(FULL, k, 0);
     if (k >= v.K) break;
-    const int t = v.d_row[k];
-    if (t < 0) continue;
-    float* te = v.pool + static_cast<long long>(v.t_slot[t]) * v.D;
+    const int sl = v.slot[k];
+    if (sl < 0) continue;
+    float* te = v.pool + static_cast<long long>(sl) * v.D;
     const float* de = v.dets + static_cast<long long>(k) * v.D;
     if (v.D == 512) {                                   // one pass, rows held in registers
       const float4* t4 = reinterpret_cast<const float4*>(te);
@@ -623,7 +623,7 @@ __device__ void ema_work(const EmaView v) {
       ss = warp_sum(ss);
       const double nrm = sqrt(ss);
       if (!(nrm >= 1e-12) || !isfinite(nrm)) {
-        if (lane == 0) flag_error(v.err, t + 1, TF_DEGENERATE_EMBEDDING);
+        if (lane == 0) flag_error(v.err, k + 1, TF_DEGENERATE_EMBEDDING);
         continue;
       }
       float4* o4 = reinterpret_cast<float4*>(te);
@@ -646,7 +646,7 @@ __device__ void ema_work(const EmaView v) {
     ss = warp_sum(ss);
     const double nrm = sqrt(ss);
     if (!(nrm >= 1e-12) || !isfinite(nrm)) {
-      if (lane == 0) flag_error(v.err, t + 1, TF_DEGENERATE_EMBEDDING);
+      if (lane == 0) flag_error(v.err, k + 1, TF_DEGENERATE_EMBEDDING);
       continue;
     }
     __syncwarp();
@@ -655,6 +655,15 @@ __device__ void ema_work(const EmaView v) {
       te[i] = static_cast<float>(w / nrm);
     }
   }
+}
+
+// Split cluster barrier (arrive now, wait later): the leader publishes a
+// frame's EMA list and runs on while the follower CTAs apply it.
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a, Params P) {
@@ -733,6 +742,8 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
 
   __shared__ int s_warp[33];
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work, s_Efr, s_emaK, s_cmd;
+  __shared__ int s_ema_work, s_ema_err, s_ema_b;   // the follower-applied EMA of frame s_ema_b
+  int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
   // optional phase timing (tf_set_profiling): cycles per phase + counters
   __shared__ long long s_ph[32];
   long long t_mark = 0, t_sub = 0;
@@ -797,14 +808,15 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         cost_work(cv, rank * n_warps() + warp_id(), n_warps() * C);
       }
       cl.sync();                                                      // S2
-      cl.sync();                                                      // S3
+      cl.sync();                                                      // S3: EMA list published
+      // The EMA of frame b runs while the leader finishes frame b and starts
+      // frame b + 1; the next S1 orders it before that frame's costs.
       const int Ke = *L_K;
       if (Ke > 0) {
         EmaView ev;
-        ev.d_row = cl.map_shared_rank(d_row, 0);
-        ev.t_slot = cl.map_shared_rank(t_slot, 0);
-        ev.work = cl.map_shared_rank(&s_work, 0);
-        ev.err = cl.map_shared_rank(&s_err, 0);
+        ev.slot = cl.map_shared_rank(ema_slot, 0);
+        ev.work = cl.map_shared_rank(&s_ema_work, 0);
+        ev.err = cl.map_shared_rank(&s_ema_err, 0);
         ev.pool = a.trk.emb_pool + sTf * static_cast<long long>(D);
         ev.dets = a.det.emb + fKf * static_cast<long long>(D);
         ev.alpha = P.alpha;
@@ -813,10 +825,10 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         ev.D = D;
         ema_work(ev);
       }
-      cl.sync();                                                      // S4
     }
   }
-  if (tid == 0) s_cmd = 0;
+  if (tid == 0) { s_cmd = 0; s_ema_err = STATUS_CLEAR; s_ema_b = -1; s_emaK = 0; }
+  bool s3_pending = false;        // leader arrived at S3 and has not waited yet
   TrackBuf& tb = a.trk;
   const long long sT = static_cast<long long>(s) * Tm;
   if (tid == 0) {
@@ -969,7 +981,11 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     }
     __syncthreads();
     // ---- fp64 cosine cost of un-gated pairs (tf/assoc.py:34-46), cluster-wide --
-    if (C > 1) cg::this_cluster().sync();                          // S1: entries ready
+    if (C > 1) {
+      if (s3_pending) cluster_wait_acquire();                      // S3 of the previous frame
+      s3_pending = false;
+      cg::this_cluster().sync();                                   // S1: entries ready, previous EMA done
+    }
     if (gating) {
       CostView cv;
       cv.rowptr = rowptr;
@@ -991,7 +1007,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     if (tid == 0) s_work = 0;
     TF_MARK(3);
     // errors from here on finish the frame's cluster barriers, then stop
-    const bool frame_ok = (s_err == STATUS_CLEAR);
+    const bool frame_ok = (s_err == STATUS_CLEAR) && (s_ema_err == STATUS_CLEAR);
     if (frame_ok) {
 
     // ---- exact LAP (tf/assoc.py:60-87) --------------------------------------
@@ -1305,14 +1321,16 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       t_flag[t] = remove;
     }
     }  // frame_ok
-    if (tid == 0) s_emaK = frame_ok ? K : 0;
+    for (int k = tid; k < K; k += blockDim.x) ema_slot[k] = (frame_ok && d_row[k] >= 0) ? t_slot[d_row[k]] : -1;
+    if (tid == 0) { s_emaK = frame_ok ? K : 0; s_ema_work = 0; if (frame_ok) s_ema_b = b; }
     __syncthreads();
-    if (C > 1) cg::this_cluster().sync();                          // S3: matches ready
-    if (frame_ok) {
+    if (C > 1) {
+      cluster_arrive_release();                                   // S3: EMA list published
+      s3_pending = true;
+    } else if (frame_ok) {
       EmaView ev;
-      ev.d_row = d_row;
-      ev.t_slot = t_slot;
-      ev.work = &s_work;
+      ev.slot = ema_slot;
+      ev.work = &s_ema_work;
       ev.err = &s_err;
       ev.pool = a.trk.emb_pool + sT * static_cast<long long>(D);
       ev.dets = a.det.emb + fK * static_cast<long long>(D);
@@ -1321,12 +1339,14 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       ev.K = K;
       ev.D = D;
       ema_work(ev);
+      __syncthreads();
     }
-    __syncthreads();
-    if (C > 1) cg::this_cluster().sync();                          // S4: EMA done
     TF_MARK(6);
     if (!frame_ok) {                          // errors before the LAP: stop here
-      if (tid == 0) s_status = (b << 8) | (s_err & 0xff);
+      if (tid == 0) {
+        if (s_err != STATUS_CLEAR) s_status = (b << 8) | (s_err & 0xff);
+        else s_status = (s_ema_b << 8) | (s_ema_err & 0xff);  // follower EMA of the previous frame
+      }
       break;
     }
 
@@ -1462,8 +1482,10 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   if (C > 1) {
     if (tid == 0) s_cmd = 1;
     __syncthreads();
-    cg::this_cluster().sync();        // S1': followers read the stop command
+    if (s3_pending) cluster_wait_acquire();
+    cg::this_cluster().sync();        // S1': followers read the stop command (their last EMA is done)
     cg::this_cluster().sync();        // followers are done with this CTA's memory
+    if (tid == 0 && s_status == 0 && s_ema_err != STATUS_CLEAR) s_status = (s_ema_b << 8) | (s_ema_err & 0xff);
   }
   // ---- write the stream's state back -----------------------------------------
   T = s_T;
