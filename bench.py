@@ -441,10 +441,11 @@ def run_ours(args):
                 for i, name in list(enumerate(["load_predict", "gate", "csr", "cost", "lap", "match",
                                                "update_ema", "records_births"]))
                 + [(16, "lap.components_tiecheck"), (17, "lap.peeling"), (18, "lap.residual_setup"),
-                   (19, "lap.warp_solves"), (20, "lap.full_restatement")]},
+                   (19, "lap.warp_solves"), (20, "lap.full_restatement"), (21, "cost.s1_wait"),
+                   (22, "cost.leader_work"), (23, "cost.s2_wait")]},
             "assoc_counters_per_frame": {name: float(phase[i]) / max(phase[11], 1) for i, name in
                                          [(8, "tie_fallback"), (9, "finite_entries"), (10, "multi_components"),
-                                          (14, "residual_entries"), (12, "tracks"), (13, "detections")]},
+                                          (14, "residual_entries"), (12, "tracks"), (13, "detections"), (15, "peel_rounds")]},
             "ranks": per_rank,
             "gpu_launches": 2 * K * (1 if not streamed else 1) + (K if streamed else 0),
             "clocks": clocks.summary(),

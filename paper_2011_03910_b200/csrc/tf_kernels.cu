@@ -510,7 +510,7 @@ struct CostView {
   double* eval;
   const int* t_slot;
   int* work;
-  unsigned long long* amp;     // bit pattern of the (non-negative) max cost
+  double* ampw;                // per-worker max cost (one slot per cluster warp)
   const float* pool;           // this stream's embedding pool
   const float* dets;           // this frame's detection embeddings
   int T, E, D;
@@ -574,10 +574,9 @@ __device__ void cost_work(const CostView v, int worker, int n_workers) {
     amp = fmax(amp, c0);
     if (two) amp = fmax(amp, c1);
   }
-  // amplitude = max |finite| (tf/assoc.py:71); costs are >= 0, so an integer
-  // max over the bit patterns is exact
-  if (lane == 0 && amp > 0.0)
-    atomicMax(v.amp, static_cast<unsigned long long>(__double_as_longlong(amp)));
+  // amplitude = max |finite| (tf/assoc.py:71): one slot per worker, reduced
+  // by the leader (a contended u64 atomicMax over DSMEM is a CAS loop)
+  if (lane == 0) v.ampw[worker] = amp;
 }
 
 struct EmaView {
@@ -744,6 +743,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work, s_Efr, s_emaK, s_cmd;
   __shared__ int s_ema_work, s_ema_err, s_ema_b;   // the follower-applied EMA of frame s_ema_b
   int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
+
   // optional phase timing (tf_set_profiling): cycles per phase + counters
   __shared__ long long s_ph[32];
   long long t_mark = 0, t_sub = 0;
@@ -765,6 +765,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   if (tid < 32) s_ph[tid] = 0;
   __shared__ long long s_next;
   __shared__ double s_amp;
+  __shared__ double s_ampw[64];     // per-worker cost maxima (cluster warps <= 64)
 
   // Large-E overflow: entries go to this stream's global pool.
   int16_t* const smem_ecol = reinterpret_cast<int16_t*>(smem + pl.off_ecol);
@@ -799,7 +800,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         cv.eval = pooled ? a.pool_val + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(smem_eval, 0);
         cv.t_slot = cl.map_shared_rank(t_slot, 0);
         cv.work = cl.map_shared_rank(&s_work, 0);
-        cv.amp = reinterpret_cast<unsigned long long*>(cl.map_shared_rank(&s_amp, 0));
+        cv.ampw = cl.map_shared_rank(s_ampw, 0);
         cv.pool = a.trk.emb_pool + sTf * static_cast<long long>(D);
         cv.dets = a.det.emb + fKf * static_cast<long long>(D);
         cv.T = *L_T;
@@ -886,51 +887,49 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     TF_MARK(0);
 
     // ---- gate (tf/tracker.py:109-110, tf/motion.py:128-142) ----------------
+    // Each warp takes four tracks at a time and walks the detection chunks
+    // (lanes own detections). The four fp64 chains are branch-free (rows past
+    // T are clamped and masked) so they interleave; the per-track count is a
+    // plain store, no atomics.
     if (gating) {
-      // lanes own detections (measurement in registers); each warp walks its
-      // tracks four at a time so four independent fp64 chains are in flight
       const int KC = (K + 31) >> 5;
-      for (int kc = 0; kc < KC; ++kc) {
-        const int k = (kc << 5) + lane;
-        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
-        if (k < K) {
-          z0 = d_meas[4 * k];
-          z1 = d_meas[4 * k + 1];
-          z2 = d_meas[4 * k + 2];
-          z3 = d_meas[4 * k + 3];
+      const double thr = P.gate_threshold;
+      const bool maha = (P.gate_metric == 0);
+      for (int t0 = 4 * wid; t0 < T; t0 += 4 * nw) {
+        int cnt[4] = {0, 0, 0, 0};
+        for (int kc = 0; kc < KC; ++kc) {
+          const int k = (kc << 5) + lane;
+          const int kk = min(k, K - 1);
+          const double z0 = d_meas[4 * kk], z1 = d_meas[4 * kk + 1], z2 = d_meas[4 * kk + 2], z3 = d_meas[4 * kk + 3];
+          double g[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = min(t0 + u, T - 1);
+            const double* m = &t_mean[8 * t];
+            if (maha) {
+              const double* il = &g_il[4 * t];
+              const double x0 = (z0 - m[0]) * il[0];
+              const double x1 = (z1 - m[1]) * il[1];
+              const double x2 = (z2 - m[2]) * il[2];
+              const double x3 = (z3 - m[3]) * il[3];
+              g[u] = ((x0 * x0 + x1 * x1) + x2 * x2) + x3 * x3;
+            } else {
+              const double dx = m[0] - z0, dy = m[1] - z1;
+              g[u] = dx * dx + dy * dy;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool fin = k < K && t0 + u < T && !(g[u] > thr);
+            const unsigned bm = __ballot_sync(FULL, fin);
+            cnt[u] += __popc(bm);
+            if (lane == 0 && t0 + u < T) gmask[(t0 + u) * KW + kc] = bm;
+          }
         }
-        for (int t0 = 4 * wid; t0 < T; t0 += 4 * nw) {
-          bool fin[4];
+        if (lane == 0) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int t = t0 + u;
-            fin[u] = false;
-            if (t < T && k < K) {
-              const double* m = &t_mean[8 * t];
-              double g;
-              if (P.gate_metric == 0) {
-                const double* il = &g_il[4 * t];
-                const double x0 = (z0 - m[0]) * il[0];
-                const double x1 = (z1 - m[1]) * il[1];
-                const double x2 = (z2 - m[2]) * il[2];
-                const double x3 = (z3 - m[3]) * il[3];
-                g = ((x0 * x0 + x1 * x1) + x2 * x2) + x3 * x3;
-              } else {
-                const double dx = m[0] - z0, dy = m[1] - z1;
-                g = dx * dx + dy * dy;
-              }
-              fin[u] = !(g > P.gate_threshold);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int t = t0 + u;
-            const unsigned bm = __ballot_sync(FULL, fin[u]);
-            if (lane == 0 && t < T) {
-              gmask[t * KW + kc] = bm;
-              if (bm) atomicAdd(&t_flag[t], __popc(bm));
-            }
-          }
+          for (int u = 0; u < 4; ++u)
+            if (t0 + u < T) t_flag[t0 + u] = cnt[u];
         }
       }
     }
@@ -938,17 +937,29 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     TF_MARK(1);
     // ---- CSR of finite (un-gated) entries, row-major -----------------------
     if (gating) {
-      if (wid == 0) {
+      if (wid == 0) {                    // lanes own 4 consecutive rows per pass
         int carry = 0;
-        for (int t0 = 0; t0 < T; t0 += 32) {
-          int t = t0 + lane;
-          int v = t < T ? t_flag[t] : 0, incl = v;
+        for (int t0 = 0; t0 < T; t0 += 128) {
+          int v[4], sum = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int t = t0 + 4 * lane + j;
+            v[j] = t < T ? t_flag[t] : 0;
+            sum += v[j];
+          }
+          int incl = sum;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             int q = __shfl_up_sync(FULL, incl, o);
             if (lane >= o) incl += q;
           }
-          if (t < T) rowptr[t] = carry + incl - v;
+          int run = carry + incl - sum;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int t = t0 + 4 * lane + j;
+            if (t < T) rowptr[t] = run;
+            run += v[j];
+          }
           carry += __shfl_sync(FULL, incl, 31);
         }
         if (lane == 0) { rowptr[T] = carry; s_E = carry; }
@@ -963,16 +974,21 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       c_epos = pooled ? a.pool_aux + static_cast<long long>(s) * 2 * Tm * Km : smem_epos;
       c_elist = pooled ? a.pool_aux + static_cast<long long>(s) * 2 * Tm * Km + static_cast<long long>(Tm) * Km
                        : smem_elist;
-      for (int t = wid; t < T; t += nw) {
-        int pos = rowptr[t];
-        for (int w = 0; w < (K + 31) / 32; ++w) {
-          unsigned bm = gmask[t * KW + w];
-          if ((bm >> lane) & 1u) {
-            int e = pos + __popc(bm & ((1u << lane) - 1u));
-            ecol[e] = static_cast<int16_t>(w * 32 + lane);
-            erow[e] = static_cast<int16_t>(t);
-          }
-          pos += __popc(bm);
+      // one thread per (row, mask word): its entries start after the row's
+      // earlier words
+      const int KWf = (K + 31) >> 5;
+      for (int x = tid; x < T * KWf; x += blockDim.x) {
+        const int t = x / KWf, w = x - t * KWf;
+        const unsigned* row = &gmask[t * KW];
+        int e = rowptr[t];
+        for (int w2 = 0; w2 < w; ++w2) e += __popc(row[w2]);
+        unsigned bm = row[w];
+        while (bm) {
+          const int b = __ffs(bm) - 1;
+          bm &= bm - 1u;
+          ecol[e] = static_cast<int16_t>(w * 32 + b);
+          erow[e] = static_cast<int16_t>(t);
+          ++e;
         }
       }
       __syncthreads();
@@ -986,6 +1002,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       s3_pending = false;
       cg::this_cluster().sync();                                   // S1: entries ready, previous EMA done
     }
+    TF_SUB(21);
     if (gating) {
       CostView cv;
       cv.rowptr = rowptr;
@@ -994,7 +1011,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       cv.eval = eval;
       cv.t_slot = t_slot;
       cv.work = &s_work;
-      cv.amp = reinterpret_cast<unsigned long long*>(&s_amp);
+      cv.ampw = s_ampw;
       cv.pool = a.trk.emb_pool + sT * static_cast<long long>(D);
       cv.dets = a.det.emb + fK * static_cast<long long>(D);
       cv.T = T;
@@ -1003,8 +1020,18 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       cost_work(cv, wid, nw * C);
     }
     __syncthreads();
+    TF_SUB(22);
     if (C > 1) cg::this_cluster().sync();                          // S2: costs written
+    TF_SUB(23);
     if (tid == 0) s_work = 0;
+    if (wid == 0) {                       // amplitude of the finite costs (read by the LAP after barriers)
+      double m = 0.0;
+      if (s_Efr > 0)
+        for (int i = lane; i < nw * C; i += 32) m = fmax(m, s_ampw[i]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+      if (lane == 0) s_amp = m;
+    }
     TF_MARK(3);
     // errors from here on finish the frame's cluster barriers, then stop
     const bool frame_ok = (s_err == STATUS_CLEAR) && (s_ema_err == STATUS_CLEAR);
@@ -1036,6 +1063,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       // edge ids are int16 in the peeling lists: beyond that, solve the padded matrix
       const bool huge = E > 32767;
       for (; !huge;) {
+        if (a.stats && tid == 0) s_ph[15] += 1;          // peeling rounds
         for (int c = tid; c < K; c += blockDim.x) { p_cmin[c] = ~0ull; p_ccnt[c] = 0; p_cdeg[c] = 0; }
         for (int r = tid; r < T; r += blockDim.x) { p_rminb[r] = ~0ull; p_rcnt[r] = 0; p_rdeg[r] = 0; }
         if (tid == 0) s_flag = 0;
