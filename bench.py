@@ -335,7 +335,7 @@ def run_ours(args):
 
     # ---- end to end through the C ABI with pinned host buffers --------------
     e2e_steps = min(K, args.e2e_steps)
-    e2e_ms, e2e_reason = None, None
+    e2e_ms, e2e_reason, e2e_kernels = None, None, None
     if (1 + e2e_steps) * step_bytes > args.e2e_host_gb * 2**30 or streamed:
         e2e_reason = f"pinned host copy of {1 + e2e_steps} steps ({(1 + e2e_steps) * step_bytes / 2**30:.0f} GiB) " \
                      f"exceeds the {args.e2e_host_gb} GiB budget"
@@ -348,6 +348,7 @@ def run_ours(args):
         hout = bt2.host_output(F)
         bt2.update(host_batches[0], host_out=hout)            # warm-up (allocates staging)
         barrier()
+        lib.tf_set_profiling(bt2.engine.ctx, 1)
         e_start.record(stream)
         for i in range(1, 1 + e2e_steps):
             bt2.update(host_batches[i], host_out=hout, sync=False)
@@ -357,6 +358,11 @@ def run_ours(args):
         bt2.engine.finish()
         barrier()
         e2e_ms = e_start.elapsed_time(e_end)
+        f2, a2, n2 = C.c_double(), C.c_double(), C.c_int64()
+        lib.tf_kernel_times(bt2.engine.ctx, C.byref(f2), C.byref(a2), C.byref(n2))
+        e2e_kernels = {"frame_heads_ms_per_launch": f2.value / max(n2.value, 1),
+                       "associate_ms_per_launch": a2.value / max(n2.value, 1), "launches": n2.value}
+        lib.tf_set_profiling(bt2.engine.ctx, 0)
         del host_batches
     h2d = F * CONF_BYTES + (cand / K) * (16 + 4 * D) + 8 * F
     d2h = 4 * F + F * cap.max_detections * (8 + 32 + 8)
@@ -419,6 +425,7 @@ def run_ours(args):
                        "parallelism": f"streams sharded over {world} rank(s), final NCCL all_gather"},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps if e2e_ms else 0,
+                    "kernels": e2e_kernels,
                     **({"unavailable": e2e_reason} if e2e_reason else {})},
             "roofline": {"bound": "hbm", "kernel": dominant,
                          "achieved": a_gbs if dominant == "associate_kernel" else f_gbs, "peak": peak,
@@ -442,7 +449,8 @@ def run_ours(args):
                                                "update_ema", "records_births"]))
                 + [(16, "lap.components_tiecheck"), (17, "lap.peeling"), (18, "lap.residual_setup"),
                    (19, "lap.warp_solves"), (20, "lap.full_restatement"), (21, "cost.s1_wait"),
-                   (22, "cost.leader_work"), (23, "cost.s2_wait")]},
+                   (22, "cost.leader_work"), (23, "cost.s2_wait"), (24, "f.trows_issue"), (25, "f.trows_wait"),
+                   (26, "f.dets_wait"), (27, "f.cost_work"), (28, "f.s2"), (29, "f.ema")]},
             "assoc_counters_per_frame": {name: float(phase[i]) / max(phase[11], 1) for i, name in
                                          [(8, "tie_fallback"), (9, "finite_entries"), (10, "multi_components"),
                                           (14, "residual_entries"), (12, "tracks"), (13, "detections"), (15, "peel_rounds")]},
@@ -466,7 +474,7 @@ def main():
     ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--batch", type=int, default=None, help="frames per stream per update (default: config's B)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--e2e-host-gb", type=float, default=24.0)
     ap.add_argument("--cpu-frames", type=int, default=640)
     ap.add_argument("--cpu-stream-frames", type=int, default=40)

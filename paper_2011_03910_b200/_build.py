@@ -50,7 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in SOURCES:
         obj = CSRC / (Path(src).stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
+        extra = os.environ.get("TF_NVCC_EXTRA", "").split()     # experiment switches (-D...)
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stdout}\n{res.stderr}")

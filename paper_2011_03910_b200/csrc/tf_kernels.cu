@@ -525,10 +525,16 @@ __device__ void cost_work(const CostView v, int worker, int n_workers) {
   for (int e0 = 2 * worker; e0 < v.E; e0 += 2 * n_workers) {
     const bool two = e0 + 1 < v.E;
     const int e1 = two ? e0 + 1 : e0;
-    const int r0 = v.erow[e0], r1 = v.erow[e1];
-    const int k0 = v.ecol[e0], k1 = v.ecol[e1];
-    const float* te0 = v.pool + static_cast<long long>(v.t_slot[r0]) * v.D;
-    const float* te1 = v.pool + static_cast<long long>(v.t_slot[r1]) * v.D;
+    // remote (DSMEM) loads are issued per thread: lanes 0..3 fetch the indices,
+    // the slots follow, and shuffles broadcast them
+    int idx = 0;
+    if (lane < 4) idx = (lane & 1) ? ((lane & 2) ? v.ecol[e1] : v.erow[e1]) : ((lane & 2) ? v.ecol[e0] : v.erow[e0]);
+    int sl = 0;
+    if (lane == 0 || lane == 1) sl = v.t_slot[idx];
+    const int k0 = __shfl_sync(FULL, idx, 2), k1 = __shfl_sync(FULL, idx, 3);
+    const int sl0 = __shfl_sync(FULL, sl, 0), sl1 = __shfl_sync(FULL, sl, 1);
+    const float* te0 = v.pool + static_cast<long long>(sl0) * v.D;
+    const float* te1 = v.pool + static_cast<long long>(sl1) * v.D;
     const float* de0 = v.dets + static_cast<long long>(k0) * v.D;
     const float* de1 = v.dets + static_cast<long long>(k1) * v.D;
     double acc0 = 0.0, acc1 = 0.0;
@@ -598,7 +604,9 @@ __device__ void ema_work(const EmaView v) {
     if (lane == 0) k = atomicAdd(v.work, 1);
     k = __shfl_sync(FULL, k, 0);
     if (k >= v.K) break;
-    const int sl = v.slot[k];
+    int sl = 0;
+    if (lane == 0) sl = v.slot[k];           // one remote load, broadcast
+    sl = __shfl_sync(FULL, sl, 0);
     if (sl < 0) continue;
     float* te = v.pool + static_cast<long long>(sl) * v.D;
     const float* de = v.dets + static_cast<long long>(k) * v.D;
@@ -785,12 +793,16 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     const long long sTf = static_cast<long long>(s) * Tm;
     for (int b = 0;; ++b) {
       cl.sync();                                                      // S1
-      if (*L_cmd) {
+      // leader scalars: one remote load each, shared through local memory
+      __shared__ int s_fl[3];
+      if (tid == 0) { s_fl[0] = *L_cmd; s_fl[1] = *L_E; s_fl[2] = *L_T; }
+      __syncthreads();
+      if (s_fl[0]) {
         cl.sync();
         return;
       }
       const long long fKf = static_cast<long long>(ls * a.B + b) * Km;
-      const int E = *L_E;
+      const int E = s_fl[1];
       if (E > 0) {
         CostView cv;
         const bool pooled = E > a.cap_entries;
@@ -803,16 +815,19 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         cv.ampw = cl.map_shared_rank(s_ampw, 0);
         cv.pool = a.trk.emb_pool + sTf * static_cast<long long>(D);
         cv.dets = a.det.emb + fKf * static_cast<long long>(D);
-        cv.T = *L_T;
+        cv.T = s_fl[2];
         cv.E = E;
         cv.D = D;
         cost_work(cv, rank * n_warps() + warp_id(), n_warps() * C);
       }
       cl.sync();                                                      // S2
       cl.sync();                                                      // S3: EMA list published
+      __shared__ int s_fk;
+      if (tid == 0) s_fk = *L_K;
+      __syncthreads();
       // The EMA of frame b runs while the leader finishes frame b and starts
       // frame b + 1; the next S1 orders it before that frame's costs.
-      const int Ke = *L_K;
+      const int Ke = s_fk;
       if (Ke > 0) {
         EmaView ev;
         ev.slot = cl.map_shared_rank(ema_slot, 0);
