@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
 
   __shared__ int s_warp[33];
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work, s_Efr, s_emaK, s_cmd;
-  __shared__ int s_ema_work, s_ema_err, s_ema_b;   // the follower-applied EMA of frame s_ema_b
+  __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2;   // the follower-applied EMA of frame s_ema_b
   int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
 
   // optional phase timing (tf_set_profiling): cycles per phase + counters
@@ -1077,21 +1077,50 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       unsigned long long* p_rminb = reinterpret_cast<unsigned long long*>(p_rmin);
       // edge ids are int16 in the peeling lists: beyond that, solve the padded matrix
       const bool huge = E > 32767;
-      for (; !huge;) {
+      // Aggregates use 32-bit keys (the high word of the non-negative cost's
+      // bit pattern: order-preserving, so a key that is the strict minimum
+      // marks a strict value minimum) and native shared-memory atomics. A key
+      // tie only makes peeling skip a pair this round; skipped pairs stay in
+      // the residual, which is solved exactly. Forced pairs never conflict (a
+      // degree-1 row or column has one candidate partner and a strict minimum
+      // is unique), so the rule pass removes them at once. Two aggregate sets
+      // alternate by round: the rule pass reads one and resets the other, so a
+      // round costs three barriers. (The component arrays are free scratch
+      // until peeling ends.)
+      // (plain selects of shared pointers, not pointer arrays: the compiler then
+      // keeps them in the shared window -- LDS / ATOMS instead of generic ops)
+      unsigned* const km0 = reinterpret_cast<unsigned*>(p_cmin);
+      unsigned* const km1 = km0 + K;
+      unsigned* const rk0 = reinterpret_cast<unsigned*>(p_rmin);
+      unsigned* const rk1 = rk0 + T;
+      for (int c = tid; c < K; c += blockDim.x) { km0[c] = ~0u; p_ccnt[c] = 0; c_nr[c] = 0; }
+      for (int r = tid; r < T; r += blockDim.x) { rk0[r] = ~0u; p_rcnt[r] = 0; c_ne[r] = 0; }
+      if (tid == 0) { s_flag = 0; s_flag2 = 0; }
+      __syncthreads();
+      for (int round = 0; !huge; ++round) {
         if (a.stats && tid == 0) s_ph[15] += 1;          // peeling rounds
-        for (int c = tid; c < K; c += blockDim.x) { p_cmin[c] = ~0ull; p_ccnt[c] = 0; p_cdeg[c] = 0; }
-        for (int r = tid; r < T; r += blockDim.x) { p_rminb[r] = ~0ull; p_rcnt[r] = 0; p_rdeg[r] = 0; }
-        if (tid == 0) s_flag = 0;
-        __syncthreads();
+        const int cur = round & 1;
+        unsigned* km = cur ? km1 : km0;
+        unsigned* rk = cur ? rk1 : rk0;
+        int* cc = cur ? p_cdeg : p_ccnt;
+        int* rc = cur ? p_rdeg : p_rcnt;
+        int* cd = cur ? c_nc : c_nr;
+        int* rd = cur ? c_root : c_ne;
+        unsigned* kmn = cur ? km0 : km1;
+        unsigned* rkn = cur ? rk0 : rk1;
+        int* ccn = cur ? p_ccnt : p_cdeg;
+        int* rcn = cur ? p_rcnt : p_rdeg;
+        int* cdn = cur ? c_nr : c_nc;
+        int* rdn = cur ? c_ne : c_root;
         for (int e = tid; e < E; e += blockDim.x) {
           const int r = erow[e], c = ecol[e];
           if (p_ra[r] && p_ca[c]) {
-            const unsigned long long bv = static_cast<unsigned long long>(__double_as_longlong(eval[e]));
-            atomicMin(&p_cmin[c], bv);
-            atomicAdd(&p_cdeg[c], 1);
+            const unsigned key = static_cast<unsigned>(__double_as_longlong(eval[e]) >> 32);
+            atomicMin(&km[c], key);
+            atomicAdd(&cd[c], 1);
             p_crow[c] = r;                 // the row, when the degree ends up 1
-            atomicMin(&p_rminb[r], bv);
-            atomicAdd(&p_rdeg[r], 1);
+            atomicMin(&rk[r], key);
+            atomicAdd(&rd[r], 1);
             p_rc1[r] = c;                  // the column, when the degree ends up 1
           }
         }
@@ -1099,38 +1128,39 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         for (int e = tid; e < E; e += blockDim.x) {
           const int r = erow[e], c = ecol[e];
           if (p_ra[r] && p_ca[c]) {
-            const unsigned long long bv = static_cast<unsigned long long>(__double_as_longlong(eval[e]));
-            if (bv == p_cmin[c]) atomicAdd(&p_ccnt[c], 1);
-            if (bv == p_rminb[r]) atomicAdd(&p_rcnt[r], 1);
+            const unsigned key = static_cast<unsigned>(__double_as_longlong(eval[e]) >> 32);
+            if (key == km[c]) atomicAdd(&cc[c], 1);
+            if (key == rk[r]) atomicAdd(&rc[r], 1);
           }
         }
         __syncthreads();
-        for (int r = tid; r < T; r += blockDim.x)        // R1
-          if (p_ra[r] && p_rdeg[r] == 1) {
-            const int c = p_rc1[r];
-            if (p_ccnt[c] == 1 && p_rminb[r] == p_cmin[c]) {
-              rcol[r] = static_cast<int16_t>(c);
-              p_kr[r] = 1;
-              p_kc[c] = 1;
-              s_flag = 1;
+        int* flag = cur ? &s_flag2 : &s_flag;
+        if (tid == 0) *(cur ? &s_flag : &s_flag2) = 0;   // the next round's flag
+        for (int x = tid; x < T + K; x += blockDim.x) {
+          int r = -1, c = -1;
+          if (x < T) {                                    // R1
+            if (p_ra[x] && rd[x] == 1) {
+              const int c1 = p_rc1[x];
+              if (cc[c1] == 1 && rk[x] == km[c1]) { r = x; c = c1; }
+            }
+          } else {                                        // R2
+            const int cx = x - T;
+            if (p_ca[cx] && cd[cx] == 1) {
+              const int r1 = p_crow[cx];
+              if (rc[r1] == 1 && rk[r1] == km[cx]) { r = r1; c = cx; }
             }
           }
-        for (int c = tid; c < K; c += blockDim.x)        // R2
-          if (p_ca[c] && p_cdeg[c] == 1) {
-            const int r = p_crow[c];
-            if (p_rcnt[r] == 1 && p_rminb[r] == p_cmin[c]) {
-              rcol[r] = static_cast<int16_t>(c);
-              p_kr[r] = 1;
-              p_kc[c] = 1;
-              s_flag = 1;
-            }
+          if (r >= 0) {
+            rcol[r] = static_cast<int16_t>(c);
+            p_ra[r] = 0;
+            p_ca[c] = 0;
+            *flag = 1;
           }
+        }
+        for (int cx = tid; cx < K; cx += blockDim.x) { kmn[cx] = ~0u; ccn[cx] = 0; cdn[cx] = 0; }
+        for (int rx = tid; rx < T; rx += blockDim.x) { rkn[rx] = ~0u; rcn[rx] = 0; rdn[rx] = 0; }
         __syncthreads();
-        const int go = s_flag;
-        for (int r = tid; r < T; r += blockDim.x) if (p_kr[r]) { p_ra[r] = 0; p_kr[r] = 0; }
-        for (int c = tid; c < K; c += blockDim.x) if (p_kc[c]) { p_ca[c] = 0; p_kc[c] = 0; }
-        __syncthreads();
-        if (!go) break;
+        if (!*flag) break;
       }
       TF_SUB(17);
       // residual edges, compacted in CSR order
