@@ -299,6 +299,37 @@ __device__ int block_rank(int n, FlagFn flag, int16_t* pos, int* sh_warp /* [33]
   return base;
 }
 
+// Block-wide exclusive scan of one 64-bit word per thread (callers pack four
+// 16-bit counters into it, so four ranks cost one scan). Returns the exclusive
+// prefix; *total gets the block total. All threads must call; `sh` [33] may be
+// reused only after another barrier.
+__device__ inline unsigned long long block_exscan_u64(unsigned long long v, unsigned long long* sh,
+                                                     unsigned long long* total) {
+  const int lane = lane_id(), wid = warp_id(), nw = n_warps();
+  unsigned long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) sh[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const unsigned long long x = lane < nw ? sh[lane] : 0ull;
+    unsigned long long xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(FULL, xi, o);
+      if (lane >= o) xi += t;
+    }
+    if (lane < nw) sh[lane] = xi - x;
+    if (lane == 31) sh[32] = xi;
+  }
+  __syncthreads();
+  *total = sh[32];
+  return sh[wid] + incl - v;
+}
+
 // ---------------------------------------------------------------- warp LAP
 // Exact restatement of the solver behind hungarian_solve (tf/assoc.py:60-87 ->
 // scipy.optimize.linear_sum_assignment, Crouse's shortest augmenting path; see

@@ -748,6 +748,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   for (int x = threadIdx.x; x < Km; x += blockDim.x) p_kc[x] = 0;
 
   __shared__ int s_warp[33];
+  __shared__ unsigned long long s_scan64[33];
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work, s_Efr, s_emaK, s_cmd;
   __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2;   // the follower-applied EMA of frame s_ema_b
   int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
@@ -1424,59 +1425,85 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     }
 
     // ---- records: matched tracks in list (= id) order, then births ---------
-    // Births are unmatched detections in ascending order (tf/tracker.py:145-157).
-    const int n_rec_matched = block_rank(T, [&](int t) { return t_mdet[t] >= 0 && t_hits[t] >= P.min_hits; },
-                                         npos, s_warp);
-    const long long fR = static_cast<long long>(f) * a.out.max_records;
-    for (int t = tid; t < T; t += blockDim.x) {
-      const int r = npos[t];
-      const int k = t_mdet[t];
-      if (k >= 0 && a.trace.det_track) {
-        a.trace.det_track[fK + k] = t_id[t];
-        a.trace.det_cost[fK + k] = t_mcost[t];
-        a.trace.det_matched[fK + k] = 1;
-      }
-      if (r < 0) continue;
-      double box[4];
-      if (!meas_to_box(&t_mean[8 * t], box)) flag_error(&s_err, t + 1, TF_INVALID_BOX);
-      if (r < a.out.max_records) {
-        a.out.track_id[fR + r] = t_id[t];
-        for (int q = 0; q < 4; ++q) a.out.box[(fR + r) * 4 + q] = box[q];
-        a.out.objectness[fR + r] = d_obj[k];
+    // Births are unmatched detections in ascending order (tf/tracker.py:145-157);
+    // removed tracks leave the list in order (tf/tracker.py:133-143) and push
+    // their embedding slots onto the free stack. The four ranks (record,
+    // birth, removed, kept) come from one block scan of packed 16-bit counters.
+    int* rec_pos = c_nr;                       // LAP scratch, free from here on
+    unsigned long long tot4 = 0;
+    {
+      const int n_items = T > K ? T : K;
+      for (int c0 = 0; c0 < n_items; c0 += blockDim.x) {
+        const int i = c0 + tid;
+        const bool f0 = i < T && t_mdet[i] >= 0 && t_hits[i] >= P.min_hits;
+        const bool f1 = i < K && d_row[i] < 0;
+        const bool f2 = i < T && t_flag[i] != 0;
+        const bool f3 = i < T && t_flag[i] == 0;
+        const unsigned long long v = static_cast<unsigned long long>(f0) | (static_cast<unsigned long long>(f1) << 16) |
+                                     (static_cast<unsigned long long>(f2) << 32) |
+                                     (static_cast<unsigned long long>(f3) << 48);
+        unsigned long long tot;
+        const unsigned long long ex = block_exscan_u64(v, s_scan64, &tot) + tot4;
+        if (i < T) {
+          rec_pos[i] = f0 ? static_cast<int>(ex & 0xffff) : -1;
+          rpos[i] = f2 ? static_cast<int16_t>((ex >> 32) & 0xffff) : static_cast<int16_t>(-1);
+          npos[i] = f3 ? static_cast<int16_t>(ex >> 48) : static_cast<int16_t>(-1);
+        }
+        if (i < K) d_pos[i] = f1 ? static_cast<int16_t>((ex >> 16) & 0xffff) : static_cast<int16_t>(-1);
+        tot4 += tot;
+        if (c0 + static_cast<int>(blockDim.x) < n_items) __syncthreads();   // s_scan64 reuse
       }
     }
-    const int n_birth = block_rank(K, [&](int k) { return d_row[k] < 0; }, d_pos, s_warp);
-    // removed tracks, ranked in list order: their embedding slots are pushed
-    // onto the free stack (tf/tracker.py:133-143 keeps survivors in order)
-    const int n_rm = block_rank(T, [&](int t) { return t_flag[t] != 0; }, rpos, s_warp);
+    const int n_rec_matched = static_cast<int>(tot4 & 0xffff);
+    const int n_birth = static_cast<int>((tot4 >> 16) & 0xffff);
+    const int n_rm = static_cast<int>((tot4 >> 32) & 0xffff);
     const int n_surv = T - n_rm;
     if (n_surv + n_birth > Tm) {
       if (tid == 0) s_status = (b << 8) | TF_CAPACITY;
       break;
     }
+    const long long fR = static_cast<long long>(f) * a.out.max_records;
     const int base_free = s_nfree;
-    for (int t = tid; t < T; t += blockDim.x)
-      if (t_flag[t]) a.trk.free_stack[sT + base_free + rpos[t]] = t_slot[t];
-    block_rank(T, [&](int t) { return t_flag[t] == 0; }, npos, s_warp);
-    // ordered in-place compaction, one chunk of blockDim rows per round:
-    // destinations never exceed sources, and a round's reads finish before
-    // its writes, so later rounds' sources are untouched.
+    // matched records, trace, free-stack pushes, then the ordered in-place
+    // compaction one chunk of blockDim rows per round: destinations never
+    // exceed sources, and a round's reads finish before its writes
     for (int c0 = 0; c0 < T; c0 += blockDim.x) {
       const int t = c0 + tid;
-      const bool mv = t < T && t_flag[t] == 0 && npos[t] != t;
-      const int d = mv ? npos[t] : -1;
+      bool mv = false;
+      int d = -1;
       long long r_id = 0, r_lost = 0, r_last = 0;
       int r_state = 0, r_hits = 0, r_slot = 0;
       double r_mean[8], r_cov[12];
-      if (mv) {
-        r_id = t_id[t]; r_lost = t_lost[t]; r_last = t_last[t];
-        r_state = t_state[t]; r_hits = t_hits[t]; r_slot = t_slot[t];
+      if (t < T) {
+        const int k = t_mdet[t];
+        if (k >= 0 && a.trace.det_track) {
+          a.trace.det_track[fK + k] = t_id[t];
+          a.trace.det_cost[fK + k] = t_mcost[t];
+          a.trace.det_matched[fK + k] = 1;
+        }
+        const int r = rec_pos[t];
+        if (r >= 0) {
+          double box[4];
+          if (!meas_to_box(&t_mean[8 * t], box)) flag_error(&s_err, t + 1, TF_INVALID_BOX);
+          if (r < a.out.max_records) {
+            a.out.track_id[fR + r] = t_id[t];
+            for (int q = 0; q < 4; ++q) a.out.box[(fR + r) * 4 + q] = box[q];
+            a.out.objectness[fR + r] = d_obj[k];
+          }
+        }
+        if (t_flag[t]) a.trk.free_stack[sT + base_free + rpos[t]] = t_slot[t];
+        mv = t_flag[t] == 0 && npos[t] != t;
+        if (mv) {
+          d = npos[t];
+          r_id = t_id[t]; r_lost = t_lost[t]; r_last = t_last[t];
+          r_state = t_state[t]; r_hits = t_hits[t]; r_slot = t_slot[t];
 #pragma unroll
-        for (int z = 0; z < 8; ++z) r_mean[z] = t_mean[8 * t + z];
+          for (int z = 0; z < 8; ++z) r_mean[z] = t_mean[8 * t + z];
 #pragma unroll
-        for (int z = 0; z < 12; ++z) r_cov[z] = t_cov[12 * t + z];
+          for (int z = 0; z < 12; ++z) r_cov[z] = t_cov[12 * t + z];
+        }
       }
-      __syncthreads();
+      if (n_rm > 0) __syncthreads();
       if (mv) {
         t_id[d] = r_id; t_lost[d] = r_lost; t_last[d] = r_last;
         t_state[d] = r_state; t_hits[d] = r_hits; t_slot[d] = r_slot;
@@ -1485,52 +1512,55 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
 #pragma unroll
         for (int z = 0; z < 12; ++z) t_cov[12 * d + z] = r_cov[z];
       }
-      __syncthreads();
+      __syncthreads();                         // also publishes the free-stack pushes
     }
-    if (tid == 0) s_nfree = base_free + n_rm;
-    __syncthreads();
-    // births: new tracks appended in ascending detection order
+    // births: new tracks appended in ascending detection order, one warp per
+    // birth (lane 0 initialises the row, the warp copies the embedding)
     {
-      const int nf = s_nfree;
+      const int nf = base_free + n_rm;
       const long long next = s_next;
-      for (int k = tid; k < K; k += blockDim.x) {
-        const int r = d_pos[k];
-        if (r < 0) continue;
-        const int t = n_surv + r;
-        const double* z = &d_meas[4 * k];
-        if (!(z[3] > 0.0)) flag_error(&s_err, k + 1, TF_INVALID_MEASUREMENT);
-        KF::initiate(P, z, &t_mean[8 * t], &t_cov[12 * t]);
-        t_id[t] = next + r;
-        t_state[t] = 0;
-        t_hits[t] = 1;
-        t_lost[t] = -1;
-        t_last[t] = frame;
-        t_slot[t] = a.trk.free_stack[sT + nf - 1 - r];      // pop in birth order
-        if (a.trace.det_track) {
-          a.trace.det_track[fK + k] = next + r;
-          a.trace.det_cost[fK + k] = nan("");
-          a.trace.det_matched[fK + k] = 0;
-        }
-        if (1 >= P.min_hits) {
-          const int rr = n_rec_matched + r;
-          double box[4];
-          if (!meas_to_box(z, box)) flag_error(&s_err, k + 1, TF_INVALID_BOX);
-          if (rr < a.out.max_records) {
-            a.out.track_id[fR + rr] = next + r;
-            for (int q = 0; q < 4; ++q) a.out.box[(fR + rr) * 4 + q] = box[q];
-            a.out.objectness[fR + rr] = d_obj[k];
-          }
-        }
-      }
-      __syncthreads();
       TF_MARK(7);
-      // copy detection embeddings into the new tracks' slots (warp per birth)
       for (int k = wid; k < K; k += nw) {
         const int r = d_pos[k];
         if (r < 0) continue;
-        float* dst = a.trk.emb_pool + (sT + t_slot[n_surv + r]) * static_cast<long long>(D);
+        const int t = n_surv + r;
+        int slot = 0;
+        if (lane == 0) {
+          const double* z = &d_meas[4 * k];
+          if (!(z[3] > 0.0)) flag_error(&s_err, k + 1, TF_INVALID_MEASUREMENT);
+          KF::initiate(P, z, &t_mean[8 * t], &t_cov[12 * t]);
+          t_id[t] = next + r;
+          t_state[t] = 0;
+          t_hits[t] = 1;
+          t_lost[t] = -1;
+          t_last[t] = frame;
+          slot = a.trk.free_stack[sT + nf - 1 - r];          // pop in birth order
+          t_slot[t] = slot;
+          if (a.trace.det_track) {
+            a.trace.det_track[fK + k] = next + r;
+            a.trace.det_cost[fK + k] = nan("");
+            a.trace.det_matched[fK + k] = 0;
+          }
+          if (1 >= P.min_hits) {
+            const int rr = n_rec_matched + r;
+            double box[4];
+            if (!meas_to_box(z, box)) flag_error(&s_err, k + 1, TF_INVALID_BOX);
+            if (rr < a.out.max_records) {
+              a.out.track_id[fR + rr] = next + r;
+              for (int q = 0; q < 4; ++q) a.out.box[(fR + rr) * 4 + q] = box[q];
+              a.out.objectness[fR + rr] = d_obj[k];
+            }
+          }
+        }
+        slot = __shfl_sync(FULL, slot, 0);
+        float* dst = a.trk.emb_pool + (sT + slot) * static_cast<long long>(D);
         const float* src = a.det.emb + (fK + k) * static_cast<long long>(D);
-        for (int i = lane; i < D; i += 32) dst[i] = src[i];
+        if ((D & 3) == 0) {
+          for (int i = lane; i < D / 4; i += 32)
+            reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+        } else {
+          for (int i = lane; i < D; i += 32) dst[i] = src[i];
+        }
       }
       if (tid == 0) {
         s_nfree = nf - n_birth;
