@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   __shared__ int s_warp[33];
   __shared__ unsigned long long s_scan64[33];
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work, s_Efr, s_emaK, s_cmd;
-  __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2;   // the follower-applied EMA of frame s_ema_b
+  __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2, s_nlive[2], s_nmulti;   // the follower-applied EMA of frame s_ema_b
   int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
 
   // optional phase timing (tf_set_profiling): cycles per phase + counters
@@ -1096,9 +1096,15 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       unsigned* const rk1 = rk0 + T;
       for (int c = tid; c < K; c += blockDim.x) { km0[c] = ~0u; p_ccnt[c] = 0; c_nr[c] = 0; }
       for (int r = tid; r < T; r += blockDim.x) { rk0[r] = ~0u; p_rcnt[r] = 0; c_ne[r] = 0; }
-      if (tid == 0) { s_flag = 0; s_flag2 = 0; }
+      if (tid == 0) { s_flag = 0; s_flag2 = 0; s_nlive[0] = 0; s_nlive[1] = 0; }
+      for (int x = tid; x < NN; x += blockDim.x) c_lab[x] = x;   // components start from singletons
       __syncthreads();
+      // Each round's edge pass also appends the live edges to a list (even
+      // rounds: c_elist, odd: c_epos); the last round kills nothing, so its list
+      // is the residual.
+      int last_round = 0;
       for (int round = 0; !huge; ++round) {
+        last_round = round;
         if (a.stats && tid == 0) s_ph[15] += 1;          // peeling rounds
         const int cur = round & 1;
         unsigned* km = cur ? km1 : km0;
@@ -1113,17 +1119,28 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         int* rcn = cur ? p_rcnt : p_rdeg;
         int* cdn = cur ? c_nr : c_nc;
         int* rdn = cur ? c_ne : c_root;
-        for (int e = tid; e < E; e += blockDim.x) {
-          const int r = erow[e], c = ecol[e];
-          if (p_ra[r] && p_ca[c]) {
-            const unsigned key = static_cast<unsigned>(__double_as_longlong(eval[e]) >> 32);
-            atomicMin(&km[c], key);
-            atomicAdd(&cd[c], 1);
-            p_crow[c] = r;                 // the row, when the degree ends up 1
-            atomicMin(&rk[r], key);
-            atomicAdd(&rd[r], 1);
-            p_rc1[r] = c;                  // the column, when the degree ends up 1
+        int16_t* lst = cur ? c_epos : c_elist;
+        for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+          const int e = e0 + tid;
+          bool live = false;
+          if (e < E) {
+            const int r = erow[e], c = ecol[e];
+            if (p_ra[r] && p_ca[c]) {
+              live = true;
+              const unsigned key = static_cast<unsigned>(__double_as_longlong(eval[e]) >> 32);
+              atomicMin(&km[c], key);
+              atomicAdd(&cd[c], 1);
+              p_crow[c] = r;                 // the row, when the degree ends up 1
+              atomicMin(&rk[r], key);
+              atomicAdd(&rd[r], 1);
+              p_rc1[r] = c;                  // the column, when the degree ends up 1
+            }
           }
+          const unsigned bm = __ballot_sync(FULL, live);
+          int base = 0;
+          if (lane == 0 && bm) base = atomicAdd(&s_nlive[cur], __popc(bm));
+          base = __shfl_sync(FULL, base, 0);
+          if (live) lst[base + __popc(bm & ((1u << lane) - 1u))] = static_cast<int16_t>(e);
         }
         __syncthreads();
         for (int e = tid; e < E; e += blockDim.x) {
@@ -1136,7 +1153,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         }
         __syncthreads();
         int* flag = cur ? &s_flag2 : &s_flag;
-        if (tid == 0) *(cur ? &s_flag : &s_flag2) = 0;   // the next round's flag
+        if (tid == 0) { *(cur ? &s_flag : &s_flag2) = 0; s_nlive[cur ^ 1] = 0; }   // the next round's flag, list
         for (int x = tid; x < T + K; x += blockDim.x) {
           int r = -1, c = -1;
           if (x < T) {                                    // R1
@@ -1164,57 +1181,142 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         if (!*flag) break;
       }
       TF_SUB(17);
-      // residual edges, compacted in CSR order
-      const int E_live = huge ? 0 : block_rank(E, [&](int e) { return p_ra[erow[e]] && p_ca[ecol[e]]; }, c_epos, s_warp);
-      if (!huge)
-        for (int e = tid; e < E; e += blockDim.x)
-          if (c_epos[e] >= 0) c_elist[c_epos[e]] = static_cast<int16_t>(e);
-      for (int x = tid; x < NN; x += blockDim.x) {
-        c_lab[x] = x;
-        c_nr[x] = 0;
-        c_nc[x] = 0;
-        c_ne[x] = 0;
+      // residual edges: the last peeling round's list
+      const int E_live = huge ? 0 : s_nlive[last_round & 1];
+      if (!huge && (last_round & 1)) {         // keep the residual list in c_elist
+        int16_t* tmp = c_elist;
+        c_elist = c_epos;
+        c_epos = tmp;
       }
-      if (tid == 0) { s_flag = 1; s_tie = huge; }
-      for (;;) {
+      if (tid == 0) { s_tie = huge; s_nmulti = -1; }
+      if (!huge && E_live <= 32) {
+        // Small residual (the common case): one warp labels the components,
+        // checks them for equal costs and lays out the per-component problems;
+        // no block barriers.
+        if (wid == 0) {
+          const bool on = lane < E_live;
+          int r = 0, cn = 0, root = 0;
+          double v0 = 0.0;
+          if (on) {
+            const int e = c_elist[lane];
+            r = erow[e];
+            cn = T + ecol[e];
+            v0 = eval[e];
+          }
+          for (;;) {
+            bool changed = false;
+            if (on) {
+              const int la = c_lab[r], lb = c_lab[cn];
+              if (la != lb) {
+                const int m = min(la, lb);
+                atomicMin(&c_lab[r], m);
+                atomicMin(&c_lab[cn], m);
+                changed = true;
+              }
+            }
+            __syncwarp();
+            if (on) {                                       // pointer jumping (monotone)
+              int l = c_lab[r], ll = c_lab[l];
+              if (ll < l) atomicMin(&c_lab[r], ll);
+              l = c_lab[cn]; ll = c_lab[l];
+              if (ll < l) atomicMin(&c_lab[cn], ll);
+            }
+            __syncwarp();
+            if (!__any_sync(FULL, changed)) break;
+          }
+          if (on) root = c_lab[r];
+          // equal costs inside one component -> the exact full restatement
+          bool tie = false;
+          for (int j = 1; j < 32; ++j) {
+            const int src = (lane + j) & 31;
+            const double vo = __shfl_sync(FULL, v0, src);
+            const int ro = __shfl_sync(FULL, root, src);
+            tie = tie || (on && src < E_live && ro == root && vo == v0);
+          }
+          tie = __any_sync(FULL, tie);
+          // distinct rows / columns / roots: the last writer of a marker owns it
+          int* mark = c_lrp;
+          if (on) { mark[r] = lane; mark[cn] = lane; }
+          __syncwarp();
+          const bool own_r = on && mark[r] == lane, own_c = on && mark[cn] == lane;
+          __syncwarp();
+          if (on) mark[root] = lane;
+          __syncwarp();
+          const bool own_root = on && mark[root] == lane;
+          if (own_root) { c_nr[root] = 0; c_nc[root] = 0; c_ne[root] = 0; }
+          __syncwarp();
+          if (own_r) atomicAdd(&c_nr[root], 1);
+          if (own_c) atomicAdd(&c_nc[root], 1);
+          if (on) atomicAdd(&c_ne[root], 1);
+          __syncwarp();
+          const unsigned rm = __ballot_sync(FULL, own_root);
+          const int n_multi = __popc(rm);
+          const int i = __popc(rm & ((1u << lane) - 1u));
+          const int vsz = own_root ? max(c_nr[root], c_nc[root]) : 0;
+          const int vne = own_root ? c_ne[root] : 0;
+          int isz = vsz, ine = vne;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int a1 = __shfl_up_sync(FULL, isz, o), a2 = __shfl_up_sync(FULL, ine, o);
+            if (lane >= o) { isz += a1; ine += a2; }
+          }
+          // compact the owners' (root, offsets) to slot i
+          if (own_root) {
+            c_root[i] = root;
+            c_off[i] = isz - vsz;
+            c_eoff[i] = ine - vne;
+          }
+          if (lane == 0) { s_tie = tie; s_nmulti = n_multi; }
+        }
         __syncthreads();
-        const int go = s_flag;
-        __syncthreads();
-        if (!go) break;
-        if (tid == 0) s_flag = 0;
-        __syncthreads();
+      } else {
+        for (int x = tid; x < NN; x += blockDim.x) {
+          c_lab[x] = x;
+          c_nr[x] = 0;
+          c_nc[x] = 0;
+          c_ne[x] = 0;
+        }
+        if (tid == 0) s_flag = 1;
+        for (;;) {
+          __syncthreads();
+          const int go = s_flag;
+          __syncthreads();
+          if (!go) break;
+          if (tid == 0) s_flag = 0;
+          __syncthreads();
+          for (int q = tid; q < E_live; q += blockDim.x) {
+            const int e = c_elist[q];
+            const int r = erow[e], c = T + ecol[e];
+            const int la = c_lab[r], lb = c_lab[c];
+            if (la != lb) {
+              const int m = min(la, lb);
+              atomicMin(&c_lab[r], m);
+              atomicMin(&c_lab[c], m);
+              s_flag = 1;
+            }
+          }
+          __syncthreads();
+          for (int x = tid; x < NN; x += blockDim.x) {       // pointer jumping (monotone)
+            const int l = c_lab[x], ll = c_lab[l];
+            if (ll < l) c_lab[x] = ll;
+          }
+        }
+        for (int x = tid; x < NN; x += blockDim.x) {
+          const bool alive = x < T ? p_ra[x] != 0 : p_ca[x - T] != 0;
+          if (alive) atomicAdd(x < T ? &c_nr[c_lab[x]] : &c_nc[c_lab[x]], 1);
+        }
         for (int q = tid; q < E_live; q += blockDim.x) {
           const int e = c_elist[q];
-          const int r = erow[e], c = T + ecol[e];
-          const int la = c_lab[r], lb = c_lab[c];
-          if (la != lb) {
-            const int m = min(la, lb);
-            atomicMin(&c_lab[r], m);
-            atomicMin(&c_lab[c], m);
-            s_flag = 1;
+          const int root = c_lab[erow[e]];
+          atomicAdd(&c_ne[root], 1);
+          const double v0 = eval[e];
+          for (int q2 = q + 1; q2 < E_live && !s_tie; ++q2) {
+            const int e2 = c_elist[q2];
+            if (eval[e2] == v0 && c_lab[erow[e2]] == root) s_tie = 1;
           }
         }
         __syncthreads();
-        for (int x = tid; x < NN; x += blockDim.x) {       // pointer jumping (monotone)
-          const int l = c_lab[x], ll = c_lab[l];
-          if (ll < l) c_lab[x] = ll;
-        }
       }
-      for (int x = tid; x < NN; x += blockDim.x) {
-        const bool alive = x < T ? p_ra[x] != 0 : p_ca[x - T] != 0;
-        if (alive) atomicAdd(x < T ? &c_nr[c_lab[x]] : &c_nc[c_lab[x]], 1);
-      }
-      for (int q = tid; q < E_live; q += blockDim.x) {
-        const int e = c_elist[q];
-        const int root = c_lab[erow[e]];
-        atomicAdd(&c_ne[root], 1);
-        const double v0 = eval[e];
-        for (int q2 = q + 1; q2 < E_live && !s_tie; ++q2) {
-          const int e2 = c_elist[q2];
-          if (eval[e2] == v0 && c_lab[erow[e2]] == root) s_tie = 1;
-        }
-      }
-      __syncthreads();
       TF_SUB(16);
       if (a.stats && tid == 0) { s_ph[8] += s_tie; s_ph[9] += E; s_ph[11] += 1; s_ph[12] += T; s_ph[13] += K; s_ph[14] += E_live; }
       if (s_tie) {
@@ -1230,7 +1332,10 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
           TF_SUB(20);
         }
       } else {
-        const int n_multi = block_rank(NN, [&](int x) { return c_lab[x] == x && c_ne[x] >= 1; }, c_pos, s_warp);
+        int n_multi = s_nmulti;
+        const bool laid_out = n_multi >= 0;
+        if (!laid_out) {
+        n_multi = block_rank(NN, [&](int x) { return c_lab[x] == x && c_ne[x] >= 1; }, c_pos, s_warp);
         if (a.stats && tid == 0) s_ph[10] += n_multi;
         for (int x = tid; x < NN; x += blockDim.x)
           if (c_pos[x] >= 0) c_root[c_pos[x]] = x;
@@ -1266,6 +1371,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
           }
         }
         __syncthreads();
+        }
         for (int i = wid; i < n_multi; i += nw) {
           const int root = c_root[i], off = c_off[i];
           int nr_l = 0, nc_l = 0;
