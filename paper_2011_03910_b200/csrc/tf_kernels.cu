@@ -406,9 +406,15 @@ __global__ void __launch_bounds__(512) frame_dets_kernel(RowsArgs a, Params P) {
 // Association: one persistent CTA per stream over the B frames of an update.
 // ============================================================================
 
+constexpr int kFrameTable = 64;   // frames per update whose scalars are staged in shared memory
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
 struct AssocPlan {
   size_t off_id, off_lost, off_last, off_mean, off_cov, off_mcost, off_state, off_hits,
-      off_slot, off_mdet, off_rowptr, off_flag, off_npos, off_rpos, off_dm, off_dobj, off_drow, off_dpos, off_gmask,
+      off_slot, off_mdet, off_rowptr, off_flag, off_npos, off_rpos, off_dm, off_dobj, off_dm2, off_dobj2, off_drow, off_dpos, off_gmask,
       off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
       off_vr, off_vc, off_lab, off_cnr, off_cnc, off_cne, off_croot, off_coff, off_cpos, off_crows, off_ccols,
       off_cmap, off_rcol, off_rmap, off_lrp, off_eoff, off_il, off_epos, off_elist, off_pcmin, off_prmin, off_pccnt, off_pcdeg, off_pcrow, off_prdeg, off_prcnt, off_prc1,
@@ -437,6 +443,8 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_rpos, 2 * T)
   TF_TAKE(off_dm, 8 * 4 * K)
   TF_TAKE(off_dobj, 8 * K)
+  TF_TAKE(off_dm2, 8 * 4 * K)     // second buffer: frame b + 1 is prefetched while frame b runs
+  TF_TAKE(off_dobj2, 8 * K)
   TF_TAKE(off_drow, 4 * K)
   TF_TAKE(off_dpos, 2 * K)
   TF_TAKE(off_emas, 4 * K)        // EMA work list of the frame (det -> pool slot), read by followers
@@ -697,8 +705,12 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   int* t_flag = reinterpret_cast<int*>(smem + pl.off_flag);
   int16_t* npos = reinterpret_cast<int16_t*>(smem + pl.off_npos);
   int16_t* rpos = reinterpret_cast<int16_t*>(smem + pl.off_rpos);
-  double* d_meas = reinterpret_cast<double*>(smem + pl.off_dm);
-  double* d_obj = reinterpret_cast<double*>(smem + pl.off_dobj);
+  double* const d_meas0 = reinterpret_cast<double*>(smem + pl.off_dm);
+  double* const d_obj0 = reinterpret_cast<double*>(smem + pl.off_dobj);
+  double* const d_meas1 = reinterpret_cast<double*>(smem + pl.off_dm2);
+  double* const d_obj1 = reinterpret_cast<double*>(smem + pl.off_dobj2);
+  double* d_meas = d_meas0;
+  double* d_obj = d_obj0;
   int* d_row = reinterpret_cast<int*>(smem + pl.off_drow);
   int16_t* d_pos = reinterpret_cast<int16_t*>(smem + pl.off_dpos);
   unsigned* gmask = reinterpret_cast<unsigned*>(smem + pl.off_gmask);
@@ -866,25 +878,53 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     for (int q = 0; q < 8; ++q) t_mean[8 * t + q] = tb.mean[(sT + t) * 8 + q];
     for (int q = 0; q < 12; ++q) t_cov[12 * t + q] = tb.cov[(sT + t) * 12 + q];
   }
+  // frame table of the update (index, decode status, detection count) and
+  // the first frame's detections: the per-frame scalar loads and the
+  // measurement copy leave the frame's critical path
+  __shared__ long long s_fidx[kFrameTable];
+  __shared__ int s_fst[kFrameTable], s_fcnt[kFrameTable];
+  for (int i = tid; i < a.B && i < kFrameTable; i += blockDim.x) {
+    const int fi = ls * a.B + i;
+    s_fidx[i] = a.frame_index[fi];
+    s_fst[i] = a.det.status[fi];
+    s_fcnt[i] = min(a.det.count[fi], Km);
+  }
+  auto frame_count = [&](int b) { return b < kFrameTable ? s_fcnt[b] : min(a.det.count[ls * a.B + b], Km); };
+  auto prefetch_dets = [&](int b, double* dm, double* dob) {
+    // cp.async (LDGSTS): 2 x 16 B of measurement + 8 B objectness per detection
+    const long long fKp = static_cast<long long>(ls * a.B + b) * Km;
+    const int Kp = frame_count(b);
+    for (int k = tid; k < Kp; k += blockDim.x) {
+      const double* sm = a.det.meas + (fKp + k) * 4;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dm + 4 * k)), "l"(sm) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dm + 4 * k + 2)), "l"(sm + 2) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dob + k)), "l"(a.det.obj + fKp + k) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
   __syncthreads();
+  if (a.B > 0) prefetch_dets(0, d_meas0, d_obj0);
 
   for (int b = 0; b < a.B; ++b) {
     if (s_status != 0) break;                      // stream failed earlier: stop
     const int f = ls * a.B + b;
     const long long fK = static_cast<long long>(f) * Km;
-    const long long frame = a.frame_index[f];
-    if (a.det.status[f] != 0) {                    // decode/NMS error of this frame
-      if (tid == 0) s_status = (b << 8) | a.det.status[f];
+    const long long frame = b < kFrameTable ? s_fidx[b] : a.frame_index[f];
+    const int fst = b < kFrameTable ? s_fst[b] : a.det.status[f];
+    if (fst != 0) {                                // decode/NMS error of this frame
+      if (tid == 0) s_status = (b << 8) | fst;
       break;
     }
-    const int K = a.det.count[f];
+    const int K = frame_count(b);
     T = s_T;
     if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; s_work = 0; s_Efr = 0; t_frame0 = clock64(); }
-    for (int k = tid; k < K; k += blockDim.x) {
-      for (int q = 0; q < 4; ++q) d_meas[4 * k + q] = a.det.meas[(fK + k) * 4 + q];
-      d_obj[k] = a.det.obj[fK + k];
-      d_row[k] = -1;
-    }
+    // this frame's detections were prefetched (this thread's copies land here;
+    // the predict barrier publishes all of them); start the next frame's
+    d_meas = (b & 1) ? d_meas1 : d_meas0;
+    d_obj = (b & 1) ? d_obj1 : d_obj0;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (b + 1 < a.B) prefetch_dets(b + 1, (b & 1) ? d_meas0 : d_meas1, (b & 1) ? d_obj0 : d_obj1);
+    for (int k = tid; k < K; k += blockDim.x) d_row[k] = -1;
     // ---- Kalman predict for every live track (tf/tracker.py:98-99) --------
     const bool gating = (T > 0 && K > 0);
     for (int t = tid; t < T; t += blockDim.x) {
@@ -1686,6 +1726,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       break;
     }
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");   // no prefetch outlives an early exit
   __syncthreads();
   // ---- release the follower CTAs (they wait at the S1 barrier) ----------------
   if (C > 1) {
