@@ -56,9 +56,11 @@ __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~size_t(
 
 __host__ __device__ inline FramePlan frame_plan(int total_anchors, int cap_cand, int words) {
   FramePlan p;
-  p.nchunks = (total_anchors + 31) / 32;
+  // confidence scan groups: 128 anchors of one (scale, anchor) plane each,
+  // so at most total/128 + 12 groups; four 32-bit ballots per group
+  p.nchunks = (total_anchors + 127) / 128 + 12;
   size_t o = 0;
-  p.off_masks = o;  o = align16(o + sizeof(unsigned) * p.nchunks);
+  p.off_masks = o;  o = align16(o + 16 * static_cast<size_t>(p.nchunks));
   p.off_code = o;   o = align16(o + sizeof(int) * cap_cand);
   p.off_box = o;    o = align16(o + sizeof(double) * 4 * cap_cand);
   p.off_score = o;  o = align16(o + sizeof(double) * cap_cand);
@@ -156,6 +158,8 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
   __shared__ const float* s_bg[12];
   __shared__ const float* s_fg[12];
   __shared__ int s_start[13];
+  __shared__ int s_gstart[13];           // first scan group of each plane
+  __shared__ int s_vec[12];              // plane pair is 16-byte aligned (float4 loads)
   __shared__ int s_warp[33];
   __shared__ int s_misc[4];
 
@@ -174,12 +178,23 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
         acc += a.sc[si].H * a.sc[si].W;
       }
     s_start[12] = acc;
+    int gacc = 0;
+    for (int p = 0; p < 12; ++p) {
+      s_gstart[p] = gacc;
+      gacc += (s_start[p + 1] - s_start[p] + 127) / 128;
+    }
+    s_gstart[12] = gacc;
     s_misc[0] = STATUS_CLEAR;
+  }
+  __syncthreads();
+  if (tid < 12) {
+    const int hw = s_start[tid + 1] - s_start[tid];
+    s_vec[tid] = ((reinterpret_cast<uintptr_t>(s_bg[tid]) | reinterpret_cast<uintptr_t>(s_fg[tid])) & 15) == 0 &&
+                 (hw & 3) == 0;
   }
   __syncthreads();
   const int total = s_start[12];
   const FramePlan plan = frame_plan(total, a.cap_cand, a.words);
-  unsigned* masks = reinterpret_cast<unsigned*>(smem + plan.off_masks);
   int* ccode = reinterpret_cast<int*>(smem + plan.off_code);
   double* cbox = reinterpret_cast<double*>(smem + plan.off_box);
   double* cscore = reinterpret_cast<double*>(smem + plan.off_score);
@@ -189,37 +204,58 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
   uint8_t* ckeep = smem + plan.off_keep;
   int16_t* cpos = reinterpret_cast<int16_t*>(smem + plan.off_pos);
 
-  // ---- pass 1: confidence scan, one ballot mask per 32 anchors -------------
-  const int nch = plan.nchunks;
-  const int per_warp = (nch + nw - 1) / nw;
-  const int c0 = wid * per_warp, c1 = min(nch, c0 + per_warp);
+  // ---- pass 1: confidence scan ---------------------------------------------
+  // The 12 (scale, anchor) background / foreground plane pairs are split into
+  // groups of 128 anchors; a lane owns 4 consecutive anchors (one float4 of
+  // each plane when the planes are 16-byte aligned) and a warp keeps TF_SCAN_U
+  // groups of loads in flight. Each group stores four ballots (bit l of
+  // ballot i = anchor 4l + i) so pass 2 ranks candidates without re-reading.
+  const uint4* gmask_ro = reinterpret_cast<const uint4*>(smem + plan.off_masks);
+  uint4* gmasks = reinterpret_cast<uint4*>(smem + plan.off_masks);
+  const int NG = s_gstart[12];
+  const int per_warp = (NG + nw - 1) / nw;
+  const int g0 = min(NG, wid * per_warp), g1 = min(NG, g0 + per_warp);
   const double lim = P.conf_logit;
   int count = 0;
-  int pl = 0;
   constexpr int U = 4;
-  for (int c = c0; c < c1; c += U) {
-    float bg[U], fg[U];
-    bool valid[U];
+  {
+    int pl = 0;
+    for (int g = g0; g < g1; g += U) {
+      float4 bgv[U], fgv[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      int g = (c + k) * 32 + lane;
-      valid[k] = (c + k < c1) && (g < total);
-      bg[k] = 0.f;
-      fg[k] = -INFINITY;
-      if (valid[k]) {
-        while (g >= s_start[pl + 1]) ++pl;
-        int pos = g - s_start[pl];
-        bg[k] = __ldcs(s_bg[pl] + pos);
-        fg[k] = __ldcs(s_fg[pl] + pos);
+      for (int k = 0; k < U; ++k) {
+        const int gg = g + k;
+        bgv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        fgv[k] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (gg < g1) {
+          while (gg >= s_gstart[pl + 1]) ++pl;
+          const int hw = s_start[pl + 1] - s_start[pl];
+          const int pos = (gg - s_gstart[pl]) * 128 + 4 * lane;
+          if (s_vec[pl]) {
+            if (pos < hw) {
+              bgv[k] = __ldcs(reinterpret_cast<const float4*>(s_bg[pl] + pos));
+              fgv[k] = __ldcs(reinterpret_cast<const float4*>(s_fg[pl] + pos));
+            }
+          } else {
+            const float* pb = s_bg[pl] + pos;
+            const float* pf = s_fg[pl] + pos;
+            if (pos < hw) { bgv[k].x = __ldcs(pb); fgv[k].x = __ldcs(pf); }
+            if (pos + 1 < hw) { bgv[k].y = __ldcs(pb + 1); fgv[k].y = __ldcs(pf + 1); }
+            if (pos + 2 < hw) { bgv[k].z = __ldcs(pb + 2); fgv[k].z = __ldcs(pf + 2); }
+            if (pos + 3 < hw) { bgv[k].w = __ldcs(pb + 3); fgv[k].w = __ldcs(pf + 3); }
+          }
+        }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      if (c + k >= c1) break;
-      bool keep = valid[k] && ((static_cast<double>(fg[k]) - static_cast<double>(bg[k])) >= lim);
-      unsigned m = __ballot_sync(FULL, keep);
-      if (lane == 0) masks[c + k] = m;
-      count += __popc(m);
+      for (int k = 0; k < U; ++k) {
+        if (g + k >= g1) break;
+        const unsigned m0 = __ballot_sync(FULL, (static_cast<double>(fgv[k].x) - static_cast<double>(bgv[k].x)) >= lim);
+        const unsigned m1 = __ballot_sync(FULL, (static_cast<double>(fgv[k].y) - static_cast<double>(bgv[k].y)) >= lim);
+        const unsigned m2 = __ballot_sync(FULL, (static_cast<double>(fgv[k].z) - static_cast<double>(bgv[k].z)) >= lim);
+        const unsigned m3 = __ballot_sync(FULL, (static_cast<double>(fgv[k].w) - static_cast<double>(bgv[k].w)) >= lim);
+        if (lane == 0) gmasks[g + k] = make_uint4(m0, m1, m2, m3);
+        count += __popc(m0) + __popc(m1) + __popc(m2) + __popc(m3);
+      }
     }
   }
   if (lane == 0) s_warp[wid] = count;
@@ -239,17 +275,23 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
   const int C = min(C_all, a.cap_cand);
   if (tid == 0 && C_all > a.cap_cand) flag_error(&s_misc[0], 0, TF_CAPACITY);
 
-  // ---- pass 2: ordered compaction of candidate codes -----------------------
+  // ---- pass 2: ordered compaction of candidate codes (anchor order) --------
   {
     int base = s_warp[wid];
-    for (int c = c0; c < c1; ++c) {
-      unsigned m = masks[c];
-      if (m == 0u) continue;
-      if ((m >> lane) & 1u) {
-        int r = base + __popc(m & ((1u << lane) - 1u));
-        if (r < C) ccode[r] = c * 32 + lane;
-      }
-      base += __popc(m);
+    int pl = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int gg = g0; gg < g1; ++gg) {
+      const uint4 m = gmask_ro[gg];
+      const int tot = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
+      if (tot == 0) continue;
+      while (gg >= s_gstart[pl + 1]) ++pl;
+      int r = base + __popc(m.x & lt) + __popc(m.y & lt) + __popc(m.z & lt) + __popc(m.w & lt);
+      const int a0 = s_start[pl] + (gg - s_gstart[pl]) * 128 + 4 * lane;
+      if ((m.x >> lane) & 1u) { if (r < C) ccode[r] = a0; ++r; }
+      if ((m.y >> lane) & 1u) { if (r < C) ccode[r] = a0 + 1; ++r; }
+      if ((m.z >> lane) & 1u) { if (r < C) ccode[r] = a0 + 2; ++r; }
+      if ((m.w >> lane) & 1u) { if (r < C) ccode[r] = a0 + 3; ++r; }
+      base += tot;
     }
   }
   __syncthreads();
