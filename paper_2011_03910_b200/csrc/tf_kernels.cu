@@ -947,7 +947,13 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   __syncthreads();
   if (a.B > 0) prefetch_dets(0, d_meas0, d_obj0);
 
+  long long t_top = 0;
   for (int b = 0; b < a.B; ++b) {
+    if (a.stats && tid == 0) {                     // whole-frame cycles (slot 31)
+      const long long now_ = clock64();
+      if (b > 0) s_ph[31] += now_ - t_top;
+      t_top = now_;
+    }
     if (s_status != 0) break;                      // stream failed earlier: stop
     const int f = ls * a.B + b;
     const long long fK = static_cast<long long>(f) * Km;
@@ -1708,7 +1714,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       const int nf = base_free + n_rm;
       const long long next = s_next;
       TF_MARK(7);
-      for (int k = wid; k < K; k += nw) {
+      for (int k = wid; k < K; k += nw) {   // (births + frame tail: slot 30)
         const int r = d_pos[k];
         if (r < 0) continue;
         const int t = n_surv + r;
@@ -1763,6 +1769,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       }
     }
     __syncthreads();
+    TF_SUB(30);
     if (s_err != STATUS_CLEAR) {
       if (tid == 0) s_status = (b << 8) | (s_err & 0xff);
       break;
@@ -2310,8 +2317,11 @@ int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entri
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // every stream's cluster must be resident at once (clusters live inside a
+    // GPC; a second wave would double the update time): shrink until they fit
     int clusters = 0;
-    while (c > 1 && (cudaOccupancyMaxActiveClusters(&clusters, associate_kernel, &cfg) != cudaSuccess || clusters < 1)) {
+    while (c > 1 && (cudaOccupancyMaxActiveClusters(&clusters, associate_kernel, &cfg) != cudaSuccess ||
+                     clusters < n_streams)) {
       c >>= 1;
       cfg.gridDim = dim3(static_cast<unsigned>(c));
       attr[0].val.clusterDim.x = static_cast<unsigned>(c);
