@@ -360,7 +360,10 @@ def run_ours(args):
         e2e_ms = e_start.elapsed_time(e_end)
         f2, a2, n2 = C.c_double(), C.c_double(), C.c_int64()
         lib.tf_kernel_times(bt2.engine.ctx, C.byref(f2), C.byref(a2), C.byref(n2))
-        e2e_kernels = {"frame_heads_ms_per_launch": f2.value / max(n2.value, 1),
+        h2 = C.c_double()
+        lib.tf_copy_times(bt2.engine.ctx, C.byref(h2))
+        e2e_kernels = {"h2d_ms_per_step": h2.value / max(n2.value, 1),
+                       "frame_heads_ms_per_launch": f2.value / max(n2.value, 1),
                        "associate_ms_per_launch": a2.value / max(n2.value, 1), "launches": n2.value}
         lib.tf_set_profiling(bt2.engine.ctx, 0)
         del host_batches

@@ -202,6 +202,9 @@ int tf_export_tracks(tf_ctx* ctx, int32_t stream, tf_track_export* out, void* cu
  * call, and resets the accumulators. */
 int tf_set_profiling(tf_ctx* ctx, int32_t enabled);
 int tf_kernel_times(tf_ctx* ctx, double* frame_ms, double* assoc_ms, int64_t* updates);
+/* Host->device copy milliseconds (pinned-host updates) summed over the window
+ * read by the last tf_kernel_times call. */
+int tf_copy_times(tf_ctx* ctx, double* h2d_ms);
 /* Per-phase SM cycles of associate_kernel summed over streams since profiling
  * was enabled (synchronising; resets): [0] load+predict [1] gate [2] CSR
  * [3] cosine cost [4] LAP [5] matches [6] Kalman update + EMA [7] records,

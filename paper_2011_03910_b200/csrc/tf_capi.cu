@@ -69,6 +69,7 @@ struct tf_ctx {
   int profiling;
   std::vector<cudaEvent_t> events;   // triples: before frame kernel, after it, after associate
   size_t events_used;
+  double last_h2d_ms;              // host->device copy time of the last tf_kernel_times window
   long long prof_bytes_frame, prof_frames;
   long long* d_stats;
   int cluster_key, cluster_val;   // cached cluster size for the last stream count
@@ -227,7 +228,7 @@ cudaError_t prof_mark(tf_ctx* c, int which, cudaStream_t st) {
     c->events.push_back(e);
   }
   cudaError_t r = cudaEventRecord(c->events[idx], st);
-  if (which == 3) c->events_used += 4;
+  if (which == 3) c->events_used += 6;   // per update: frame, association, host->device copy
   return r;
 }
 
@@ -446,9 +447,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   const int par = c->pipeline ? c->parity : 0;
   if (c->pipeline) c->parity ^= 1;
   cudaStream_t ast = c->pipeline ? c->side : st;           // association + outputs
-  if (c->pipeline && c->asc_pending[par]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[par], 0));
   DetBuf& det = c->dets[par];
-  TF_CUDA(c, upload_frame_index(c, c->d_fidx[par], reinterpret_cast<const long long*>(frame_index), F, st));
 
   HeadLaunch h;
   h.heads = heads;
@@ -457,14 +456,30 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   h.cap_det = c->cap.max_detections;
   h.det = det;
   tf_heads staged = *heads;
+  TF_CUDA(c, prof_mark(c, 4, st));
   if (heads->host_memory) {
-    // Confidence planes (channels 4,5 of every anchor) go over PCIe with the copy
-    // engine; box deltas of candidates and the embeddings of every candidate are
-    // read in place through the mapped host pointer by the frame kernel.
+    // Default: the frame kernel reads everything it needs -- the confidence
+    // planes (coalesced float4 streams), the deltas of candidates and the
+    // embeddings of candidates -- in place through the mapped host pointer,
+    // ~17 MB per 32 frames at PCIe rate (B200 box: ~42 GB/s). The alternative
+    // (TF_HOST_CONF=copy) stages the confidence planes with a strided
+    // cudaMemcpy2DAsync; its throughput varied between 6 and 37 GB/s across
+    // boxes while plain SM reads did not, so it is opt-in.
+    const char* conf_env = getenv("TF_HOST_CONF");
+    const bool conf_mapped = !(conf_env && conf_env[0] == 'c');
     for (int i = 0; i < 3; ++i) {
       const tf_head_scale& s = heads->scale[i];
       const size_t hw = static_cast<size_t>(s.height) * s.width;
       const size_t need = static_cast<size_t>(F) * 24 * hw;
+      if (conf_mapped) {           // the frame kernel streams the planes over PCIe itself
+        void* hp = nullptr;
+        TF_CUDA(c, cudaHostGetDevicePointer(&hp, const_cast<float*>(s.head), 0));
+        h.head_ptr[i] = static_cast<const float*>(hp);
+        void* dptr = nullptr;
+        TF_CUDA(c, cudaHostGetDevicePointer(&dptr, const_cast<float*>(s.emb), 0));
+        h.emb_ptr[i] = static_cast<const float*>(dptr);
+        continue;
+      }
       if (c->stage_conf_elems[par][i] < need) {
         float* p = nullptr;
         TF_CUDA(c, dev_alloc(c, &p, need));
@@ -515,6 +530,13 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
       h.delta_stride_c[i] = heads->scale[i].head_stride_c;
     }
   }
+  TF_CUDA(c, prof_mark(c, 5, st));
+  // The confidence-plane copy above only needs the previous decode on `st` to
+  // be done with the staging buffer; the detection buffers and frame indices
+  // of this parity are read by the association two updates back, so only the
+  // decode waits for it (the copy overlaps that association).
+  if (c->pipeline && c->asc_pending[par]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[par], 0));
+  TF_CUDA(c, upload_frame_index(c, c->d_fidx[par], reinterpret_cast<const long long*>(frame_index), F, st));
   TF_CUDA(c, prof_mark(c, 0, st));
   TF_CUDA(c, launch_frame_heads(h, c->P, st));
   TF_CUDA(c, prof_mark(c, 1, st));
@@ -736,19 +758,29 @@ int tf_phase_stats(tf_ctx* c, int64_t* out16) {
   return TF_OK;
 }
 
+int tf_copy_times(tf_ctx* c, double* h2d_ms) {
+  if (!c || !h2d_ms) return TF_ARGUMENT;
+  *h2d_ms = c->last_h2d_ms;
+  return TF_OK;
+}
+
 int tf_kernel_times(tf_ctx* c, double* frame_ms, double* assoc_ms, int64_t* updates) {
   if (!c || !frame_ms || !assoc_ms || !updates) return TF_ARGUMENT;
   *frame_ms = 0.0;
   *assoc_ms = 0.0;
-  *updates = static_cast<int64_t>(c->events_used / 4);
+  *updates = static_cast<int64_t>(c->events_used / 6);
+  c->last_h2d_ms = 0.0;
   if (c->events_used == 0) return TF_OK;
-  TF_CUDA(c, cudaEventSynchronize(c->events[c->events_used - 1]));
-  for (size_t i = 0; i + 3 < c->events_used; i += 4) {
-    float a = 0.f, b = 0.f;
+  TF_CUDA(c, cudaEventSynchronize(c->events[c->events_used - 3]));
+  for (size_t i = 0; i + 5 < c->events_used; i += 6) {
+    float a = 0.f, b = 0.f, h = 0.f;
+    TF_CUDA(c, cudaEventSynchronize(c->events[i + 3]));
     TF_CUDA(c, cudaEventElapsedTime(&a, c->events[i], c->events[i + 1]));
     TF_CUDA(c, cudaEventElapsedTime(&b, c->events[i + 2], c->events[i + 3]));
+    TF_CUDA(c, cudaEventElapsedTime(&h, c->events[i + 4], c->events[i + 5]));
     *frame_ms += a;
     *assoc_ms += b;
+    c->last_h2d_ms += h;
   }
   c->events_used = 0;
   return TF_OK;
