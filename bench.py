@@ -268,9 +268,15 @@ def run_ours(args):
     gen = synth.make(args.config, device=dev, seed=args.seed + rank, streams=S)
     cap = p.Capacity(streams=S, max_frames=F, **CAPS[args.config])
     free, _ = torch.cuda.mem_get_info(dev)
-    step_bytes = F * FRAME_BYTES
+    esz = 2 if args.dtype == "f16" else 4          # input element bytes (f16: MIXED input mode)
+    conf_bytes = CONF_BYTES * esz // 4
+    step_bytes = F * FRAME_BYTES * esz // 4
+
+    def gen_batch():
+        b = gen.next_batch(B)
+        return b.half() if args.dtype == "f16" else b
     streamed = (W + K) * step_bytes > 0.55 * free
-    batches = None if streamed else [gen.next_batch(B) for _ in range(W + K)]
+    batches = None if streamed else [gen_batch() for _ in range(W + K)]
     torch.cuda.synchronize()
 
     pipe = not (streamed or args.no_pipeline)
@@ -279,7 +285,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def batch(i):
-        return gen.next_batch(B) if streamed else batches[i]
+        return gen_batch() if streamed else batches[i]
 
     for i in range(W):
         bt.update(batch(i), trace=streamed, sync=False)
@@ -367,7 +373,7 @@ def run_ours(args):
                        "associate_ms_per_launch": a2.value / max(n2.value, 1), "launches": n2.value}
         lib.tf_set_profiling(bt2.engine.ctx, 0)
         del host_batches
-    h2d = F * CONF_BYTES + (cand / K) * (16 + 4 * D) + 8 * F
+    h2d = F * conf_bytes + (cand / K) * esz * (4 + D) + 8 * F
     d2h = 4 * F + F * cap.max_detections * (8 + 32 + 8)
 
     # ---- max over ranks: the run's only collective ---------------------------
@@ -388,7 +394,7 @@ def run_ours(args):
         # write) + 48 B per record + 40 B per detection
         assoc_bytes_launch = F * (4 * D * kpf + 2 * 4 * D * kpf + 48 * rpf + 40 * kpf)
         assoc_launch_ms = as_ms.value / max(nup.value, 1)
-        frame_bytes_launch = F * (CONF_BYTES + cpf * (16 + 4 * D) + 4 * D * kpf + 40 * kpf)
+        frame_bytes_launch = F * (conf_bytes + cpf * esz * (4 + D) + 4 * D * kpf + 40 * kpf)
         frame_launch_ms = fr_ms.value / max(nup.value, 1)
         a_gbs = assoc_bytes_launch / (assoc_launch_ms / 1e3) / 1e9
         f_gbs = frame_bytes_launch / (frame_launch_ms / 1e3) / 1e9
@@ -420,6 +426,7 @@ def run_ours(args):
                                    f"update, 1088x608 3-scale JDE heads + 512-d embedding maps, objects "
                                    f"{cfg.objects}",
                        "frames_per_step": F * world if not multi else cfg.streams * B,
+                       "input_dtype": "fp16 (MIXED input mode)" if args.dtype == "f16" else "fp32",
                        "streams_per_rank": S, "inputs_exceed_l2": True,
                        "l2_policy": f"each step reads a fresh {step_bytes / 2**20:.0f} MB batch (> 126 MB L2)",
                        "generation": "streamed between steps, steps timed one by one" if streamed
@@ -484,6 +491,8 @@ def main():
     ap.add_argument("--ref-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="serialise decode and association")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f16"],
+                    help="head / embedding input type (f16 = MIXED-precision input mode, SURVEY 8(f))")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

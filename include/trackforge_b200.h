@@ -97,8 +97,10 @@ typedef struct tf_head_scale {
 typedef struct tf_heads {
   tf_head_scale scale[3];
   double scale_inv, pad_x, pad_y;
-  int32_t host_memory;            /* 1: head/emb are pinned HOST pointers (copied / read zero-copy) */
-  int32_t reserved;
+  int32_t host_memory;            /* 1: head/emb are pinned HOST pointers (read zero-copy) */
+  int32_t dtype;                  /* element type of head and emb: 0 fp32, 1 binary16 (MIXED
+                                     input mode; the pointers then address __half data and the
+                                     strides count __half elements) */
 } tf_heads;
 
 /* Per-frame records = TrackerOutput.records (tf/tracker.py:59-64,159):

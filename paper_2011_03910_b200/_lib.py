@@ -43,7 +43,7 @@ class TfHeadScale(C.Structure):
 
 class TfHeads(C.Structure):
     _fields_ = [("scale", TfHeadScale * 3), ("scale_inv", c_dbl), ("pad_x", c_dbl), ("pad_y", c_dbl),
-                ("host_memory", c_i32), ("reserved", c_i32)]
+                ("host_memory", c_i32), ("dtype", c_i32)]
 
 
 class TfRecords(C.Structure):

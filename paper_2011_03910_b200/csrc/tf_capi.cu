@@ -431,6 +431,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   if (out->max_records < 1) return fail(c, TF_ARGUMENT, "max_records must be >= 1");
   int rc = check_step_config(c);
   if (rc) return rc;
+  if (heads->dtype != 0 && heads->dtype != 1) return fail(c, TF_LAYOUT, "heads dtype must be 0 (fp32) or 1 (binary16)");
   for (int i = 0; i < 3; ++i) {
     const tf_head_scale& s = heads->scale[i];
     if (!s.head || !s.emb || s.height < 1 || s.width < 1 || s.head_stride_c < static_cast<long long>(s.height) * s.width)
@@ -466,7 +467,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     // cudaMemcpy2DAsync; its throughput varied between 6 and 37 GB/s across
     // boxes while plain SM reads did not, so it is opt-in.
     const char* conf_env = getenv("TF_HOST_CONF");
-    const bool conf_mapped = !(conf_env && conf_env[0] == 'c');
+    const bool conf_mapped = !(conf_env && conf_env[0] == 'c') || heads->dtype != 0;
     for (int i = 0; i < 3; ++i) {
       const tf_head_scale& s = heads->scale[i];
       const size_t hw = static_cast<size_t>(s.height) * s.width;

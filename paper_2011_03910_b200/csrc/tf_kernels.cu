@@ -73,21 +73,49 @@ __host__ __device__ inline FramePlan frame_plan(int total_anchors, int cap_cand,
   return p;
 }
 
+// Element access of the head / embedding inputs: fp32, or binary16 (the
+// MIXED-precision input mode: every fp16 value is exact in fp32 / fp64, so the
+// decode and the decisions downstream are those of the same values in fp32).
+template <typename T> struct Elt;
+template <> struct Elt<float> {
+  static constexpr int kVecBytes = 16;                 // 4 elements per vector load
+  static __device__ __forceinline__ float ld(const float* p) { return __ldg(p); }
+  static __device__ __forceinline__ float ldcs(const float* p) { return __ldcs(p); }
+  static __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  static __device__ __forceinline__ float4 ld4cs(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
+};
+template <> struct Elt<__half> {
+  static constexpr int kVecBytes = 8;
+  static __device__ __forceinline__ float ld(const __half* p) {
+    return __half2float(__ushort_as_half(__ldg(reinterpret_cast<const unsigned short*>(p))));
+  }
+  static __device__ __forceinline__ float ldcs(const __half* p) {
+    return __half2float(__ushort_as_half(__ldcs(reinterpret_cast<const unsigned short*>(p))));
+  }
+  static __device__ __forceinline__ float4 cvt(uint2 u) {
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+  static __device__ __forceinline__ float4 ld4(const __half* p) { return cvt(__ldg(reinterpret_cast<const uint2*>(p))); }
+  static __device__ __forceinline__ float4 ld4cs(const __half* p) { return cvt(__ldcs(reinterpret_cast<const uint2*>(p))); }
+};
+
 // Gather one embedding row (warp-cooperative), fp64 sum of squares, optional
 // binary16 round trip; writes the fp32 unit vector to `out` when non-null.
 // Mirrors normalize (tf/core.py:100-111) and _quantize_detection
 // (tf/pipeline.py:436-441). Returns a tf_status code (0 ok). The norm of every
 // row is checked even when `out` is null (parse_output normalises all rows).
-__device__ int gather_normalize(const float* src, long long stride, int dim, int quantize, float* out) {
+template <typename T>
+__device__ int gather_normalize(const T* src, long long stride, int dim, int quantize, float* out) {
   const int lane = lane_id();
-  const bool vec = (stride == 1) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (dim % 4 == 0) &&
+  const bool vec = (stride == 1) && ((reinterpret_cast<uintptr_t>(src) & (Elt<T>::kVecBytes - 1)) == 0) && (dim % 4 == 0) &&
                    (out == nullptr || (reinterpret_cast<uintptr_t>(out) & 15) == 0);
   double ss = 0.0;
   bool finite = true;
   if (vec) {
-    const float4* s4 = reinterpret_cast<const float4*>(src);
     for (int i = lane; i < dim / 4; i += 32) {
-      float4 q = __ldg(s4 + i);
+      float4 q = Elt<T>::ld4(src + 4 * i);
       double a = q.x, b = q.y, c = q.z, d = q.w;
       finite = finite && isfinite(q.x) && isfinite(q.y) && isfinite(q.z) && isfinite(q.w);
       ss = fma(a, a, ss);
@@ -97,7 +125,7 @@ __device__ int gather_normalize(const float* src, long long stride, int dim, int
     }
   } else {
     for (int i = lane; i < dim; i += 32) {
-      float x = __ldg(src + static_cast<long long>(i) * stride);
+      float x = Elt<T>::ld(src + static_cast<long long>(i) * stride);
       finite = finite && isfinite(x);
       double a = x;
       ss = fma(a, a, ss);
@@ -111,10 +139,9 @@ __device__ int gather_normalize(const float* src, long long stride, int dim, int
   if (!quantize) {
     if (out == nullptr) return TF_OK;
     if (vec) {
-      const float4* s4 = reinterpret_cast<const float4*>(src);
       float4* o4 = reinterpret_cast<float4*>(out);
       for (int i = lane; i < dim / 4; i += 32) {
-        float4 q = __ldg(s4 + i);
+        float4 q = Elt<T>::ld4(src + 4 * i);
         float4 r;
         r.x = static_cast<float>(static_cast<double>(q.x) / norm);
         r.y = static_cast<float>(static_cast<double>(q.y) / norm);
@@ -124,7 +151,7 @@ __device__ int gather_normalize(const float* src, long long stride, int dim, int
       }
     } else {
       for (int i = lane; i < dim; i += 32)
-        out[i] = static_cast<float>(static_cast<double>(__ldg(src + static_cast<long long>(i) * stride)) / norm);
+        out[i] = static_cast<float>(static_cast<double>(Elt<T>::ld(src + static_cast<long long>(i) * stride)) / norm);
     }
     return TF_OK;
   }
@@ -132,7 +159,7 @@ __device__ int gather_normalize(const float* src, long long stride, int dim, int
   double ss2 = 0.0;
   bool inrange = true;
   for (int i = lane; i < dim; i += 32) {
-    float u = static_cast<float>(static_cast<double>(__ldg(src + static_cast<long long>(i) * stride)) / norm);
+    float u = static_cast<float>(static_cast<double>(Elt<T>::ld(src + static_cast<long long>(i) * stride)) / norm);
     inrange = inrange && fabsf(u) <= 65504.0f;
     double h = __half2float(__float2half_rn(u));
     ss2 += h * h;
@@ -143,20 +170,21 @@ __device__ int gather_normalize(const float* src, long long stride, int dim, int
   if (n2 < 1e-12) return TF_DEGENERATE_EMBEDDING;
   if (out == nullptr) return TF_OK;
   for (int i = lane; i < dim; i += 32) {
-    float u = static_cast<float>(static_cast<double>(__ldg(src + static_cast<long long>(i) * stride)) / norm);
+    float u = static_cast<float>(static_cast<double>(Elt<T>::ld(src + static_cast<long long>(i) * stride)) / norm);
     double h = __half2float(__float2half_rn(u));
     out[i] = static_cast<float>(h / n2);
   }
   return TF_OK;
 }
 
+template <typename T>
 __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int f = blockIdx.x;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
 
-  __shared__ const float* s_bg[12];
-  __shared__ const float* s_fg[12];
+  __shared__ const T* s_bg[12];
+  __shared__ const T* s_fg[12];
   __shared__ int s_start[13];
   __shared__ int s_gstart[13];           // first scan group of each plane
   __shared__ int s_vec[12];              // plane pair is 16-byte aligned (float4 loads)
@@ -166,7 +194,7 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
   if (tid < 12) {
     int si = tid / 4, an = tid % 4;
     const ScaleDev& sc = a.sc[si];
-    const float* base = sc.head + static_cast<long long>(f) * sc.hs_n;
+    const T* base = reinterpret_cast<const T*>(sc.head) + static_cast<long long>(f) * sc.hs_n;
     s_bg[tid] = base + static_cast<long long>(6 * an + 4) * sc.hs_c;
     s_fg[tid] = base + static_cast<long long>(6 * an + 5) * sc.hs_c;
   }
@@ -189,7 +217,8 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
   __syncthreads();
   if (tid < 12) {
     const int hw = s_start[tid + 1] - s_start[tid];
-    s_vec[tid] = ((reinterpret_cast<uintptr_t>(s_bg[tid]) | reinterpret_cast<uintptr_t>(s_fg[tid])) & 15) == 0 &&
+    s_vec[tid] = ((reinterpret_cast<uintptr_t>(s_bg[tid]) | reinterpret_cast<uintptr_t>(s_fg[tid])) &
+                  (Elt<T>::kVecBytes - 1)) == 0 &&
                  (hw & 3) == 0;
   }
   __syncthreads();
@@ -233,16 +262,16 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
           const int pos = (gg - s_gstart[pl]) * 128 + 4 * lane;
           if (s_vec[pl]) {
             if (pos < hw) {
-              bgv[k] = __ldcs(reinterpret_cast<const float4*>(s_bg[pl] + pos));
-              fgv[k] = __ldcs(reinterpret_cast<const float4*>(s_fg[pl] + pos));
+              bgv[k] = Elt<T>::ld4cs(s_bg[pl] + pos);
+              fgv[k] = Elt<T>::ld4cs(s_fg[pl] + pos);
             }
           } else {
-            const float* pb = s_bg[pl] + pos;
-            const float* pf = s_fg[pl] + pos;
-            if (pos < hw) { bgv[k].x = __ldcs(pb); fgv[k].x = __ldcs(pf); }
-            if (pos + 1 < hw) { bgv[k].y = __ldcs(pb + 1); fgv[k].y = __ldcs(pf + 1); }
-            if (pos + 2 < hw) { bgv[k].z = __ldcs(pb + 2); fgv[k].z = __ldcs(pf + 2); }
-            if (pos + 3 < hw) { bgv[k].w = __ldcs(pb + 3); fgv[k].w = __ldcs(pf + 3); }
+            const T* pb = s_bg[pl] + pos;
+            const T* pf = s_fg[pl] + pos;
+            if (pos < hw) { bgv[k].x = Elt<T>::ldcs(pb); fgv[k].x = Elt<T>::ldcs(pf); }
+            if (pos + 1 < hw) { bgv[k].y = Elt<T>::ldcs(pb + 1); fgv[k].y = Elt<T>::ldcs(pf + 1); }
+            if (pos + 2 < hw) { bgv[k].z = Elt<T>::ldcs(pb + 2); fgv[k].z = Elt<T>::ldcs(pf + 2); }
+            if (pos + 3 < hw) { bgv[k].w = Elt<T>::ldcs(pb + 3); fgv[k].w = Elt<T>::ldcs(pf + 3); }
           }
         }
       }
@@ -305,14 +334,14 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
     const ScaleDev& sc = a.sc[si];
     const int pos = g - s_start[p];
     const int y = pos / sc.W, x = pos - y * sc.W;
-    const float* base = sc.head + static_cast<long long>(f) * sc.hs_n + pos;
-    const float* dbase = sc.delta + static_cast<long long>(f) * sc.ds_n + pos;
-    const double tx = __ldg(dbase + (6 * an + 0) * sc.ds_c);
-    const double ty = __ldg(dbase + (6 * an + 1) * sc.ds_c);
-    const double tw = __ldg(dbase + (6 * an + 2) * sc.ds_c);
-    const double th = __ldg(dbase + (6 * an + 3) * sc.ds_c);
-    const double xl = static_cast<double>(__ldg(base + (6 * an + 5) * sc.hs_c)) -
-                      static_cast<double>(__ldg(base + (6 * an + 4) * sc.hs_c));
+    const T* base = reinterpret_cast<const T*>(sc.head) + static_cast<long long>(f) * sc.hs_n + pos;
+    const T* dbase = reinterpret_cast<const T*>(sc.delta) + static_cast<long long>(f) * sc.ds_n + pos;
+    const double tx = Elt<T>::ld(dbase + (6 * an + 0) * sc.ds_c);
+    const double ty = Elt<T>::ld(dbase + (6 * an + 1) * sc.ds_c);
+    const double tw = Elt<T>::ld(dbase + (6 * an + 2) * sc.ds_c);
+    const double th = Elt<T>::ld(dbase + (6 * an + 3) * sc.ds_c);
+    const double xl = static_cast<double>(Elt<T>::ld(base + (6 * an + 5) * sc.hs_c)) -
+                      static_cast<double>(Elt<T>::ld(base + (6 * an + 4) * sc.hs_c));
     double cx = (static_cast<double>(x) + 1.0 / (1.0 + exp(-tx))) * static_cast<double>(sc.stride);
     double cy = (static_cast<double>(y) + 1.0 / (1.0 + exp(-ty))) * static_cast<double>(sc.stride);
     double bw = static_cast<double>(sc.aw[an]) * exp(tw);
@@ -362,7 +391,7 @@ __global__ void __launch_bounds__(512) frame_heads_kernel(FrameArgs a, Params P)
     const ScaleDev& sc = a.sc[p >> 2];
     const int pos = g - s_start[p];
     const int y = pos / sc.W, x = pos - y * sc.W;
-    const float* src = sc.emb + static_cast<long long>(f) * sc.es_n + static_cast<long long>(y) * sc.es_h +
+    const T* src = reinterpret_cast<const T*>(sc.emb) + static_cast<long long>(f) * sc.es_n + static_cast<long long>(y) * sc.es_h +
                        static_cast<long long>(x) * sc.es_w;
     int k = cpos[r];
     float* out = (k >= 0 && k < K) ? a.det.emb + (fbase + k) * D : nullptr;
@@ -2243,8 +2272,13 @@ cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_
   int total = 0;
   for (int i = 0; i < 3; ++i) total += 4 * h.heads->scale[i].height * h.heads->scale[i].width;
   const size_t smem = frame_smem_bytes(total, h.cap_cand);
-  cudaFuncSetAttribute(frame_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  frame_heads_kernel<<<h.frames, 512, smem, st>>>(a, P);
+  if (h.heads->dtype == 1) {          // binary16 heads and embedding maps
+    cudaFuncSetAttribute(frame_heads_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    frame_heads_kernel<__half><<<h.frames, 512, smem, st>>>(a, P);
+  } else {
+    cudaFuncSetAttribute(frame_heads_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    frame_heads_kernel<float><<<h.frames, 512, smem, st>>>(a, P);
+  }
   return cudaGetLastError();
 }
 

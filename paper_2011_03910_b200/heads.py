@@ -55,6 +55,15 @@ class HeadOutputs:
     def frames(self) -> int:
         return int(self.heads[0].shape[0])
 
+    def half(self) -> "HeadOutputs":
+        """binary16 copy (the MIXED-precision input mode: heads emitted in fp16
+        by the network), keeping each tensor's memory format."""
+        import torch
+        fmt = [torch.channels_last if e.is_contiguous(memory_format=torch.channels_last) and not e.is_contiguous()
+               else torch.contiguous_format for e in self.embs]
+        return HeadOutputs(tuple(h.half() for h in self.heads),
+                           tuple(e.half().contiguous(memory_format=m) for e, m in zip(self.embs, fmt)))
+
 
 @dataclass
 class OnlineTracks:
@@ -77,6 +86,12 @@ class OnlineTracks:
                                               else self.objectness[f, :n]))
 
 
+def _dtype_code(t) -> int | None:
+    """tf_heads.dtype of a head / embedding tensor: 0 fp32, 1 binary16 (the
+    MIXED-precision input mode, network heads emitted in fp16); None otherwise."""
+    return {"torch.float32": 0, "torch.float16": 1}.get(str(t.dtype))
+
+
 def _scale_desc(head, emb, stride: int) -> _lib.TfHeadScale:
     h, w = GRID[stride]
     if tuple(head.shape[1:]) != (24, h, w):
@@ -84,8 +99,10 @@ def _scale_desc(head, emb, stride: int) -> _lib.TfHeadScale:
     if tuple(emb.shape[2:]) != (h, w) or emb.shape[0] != head.shape[0]:
         raise LayoutError(f"embedding map of stride {stride} must be [N, D, {h}, {w}], got {tuple(emb.shape)}")
     hs = head.stride()
-    if hs[3] != 1 or hs[2] != w or head.dtype.itemsize != 4 or emb.dtype.itemsize != 4:
-        raise LayoutError("head planes must be fp32 with contiguous H*W planes")
+    if hs[3] != 1 or hs[2] != w:
+        raise LayoutError("head planes must have contiguous H*W planes")
+    if _dtype_code(head) is None or emb.dtype != head.dtype:
+        raise LayoutError(f"heads and embedding maps must both be float32 or both float16, got {head.dtype}/{emb.dtype}")
     es = emb.stride()
     d = _lib.TfHeadScale(head=head.data_ptr(), head_stride_n=hs[0], head_stride_c=hs[1], emb=emb.data_ptr(),
                          emb_stride_n=es[0], emb_stride_c=es[1], emb_stride_h=es[2], emb_stride_w=es[3],
@@ -102,6 +119,7 @@ def heads_descriptor(out: HeadOutputs, host_memory: bool) -> _lib.TfHeads:
         desc.scale[i] = _scale_desc(out.heads[i], out.embs[i], s)
     desc.scale_inv, desc.pad_x, desc.pad_y = letterbox()
     desc.host_memory = int(host_memory)
+    desc.dtype = _dtype_code(out.heads[0])
     return desc
 
 

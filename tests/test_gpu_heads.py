@@ -25,7 +25,7 @@ def _pkg():
 
 
 def _run_parity(cfg_name, steps, B, streams=1, quantize=False, literal=False, config=None, max_tracks=256,
-                **synth_kw):
+                half=False, **synth_kw):
     p, synth = _pkg()
     cfg = config or p.TrackerConfig()
     gen = synth.make(cfg_name, device="cuda", streams=streams, literal_noise=literal, **synth_kw)
@@ -36,6 +36,8 @@ def _run_parity(cfg_name, steps, B, streams=1, quantize=False, literal=False, co
     frame = 0
     for step in range(steps):
         out = gen.next_batch(B)
+        if half:
+            out = out.half()
         fidx = np.array([[frame + b for b in range(B)] for _ in range(streams)], np.int64)
         res = bt.update(out, fidx, trace=True)
         tr = {k: v.cpu().numpy() for k, v in bt.trace(streams * B).items()}
@@ -216,3 +218,24 @@ def test_pipelined_updates_match_serial():
         for f in range(8):
             n = int(c0[f])
             assert np.array_equal(i0[f, :n], i1[f, :n])
+
+
+def test_native_fp16_inputs():
+    """MIXED-precision input mode: binary16 head tensors
+    and embedding maps are read natively (half the input bytes). Every fp16
+    value is exact in fp32/fp64, so the oracle decodes the same fp16 arrays
+    and the decisions must stay bit-exact."""
+    cmp = _run_parity("cfg1", steps=2, B=16, half=True)
+    assert cmp.matches > 500
+    cmp = _run_parity("cfg0", steps=10, B=4, half=True, quantize=True)
+    assert cmp.matches > 100
+
+
+def test_fp16_layout_errors():
+    p, synth = _pkg()
+    gen = synth.make("cfg0", device="cuda")
+    out = gen.next_batch(2)
+    mixed = p.HeadOutputs(tuple(h.half() for h in out.heads), out.embs)   # fp16 heads, fp32 maps
+    bt = p.BatchTracker(1, frames_per_update=2)
+    with pytest.raises(p.LayoutError):
+        bt.update(mixed)
