@@ -176,6 +176,21 @@ int tf_update_heads(tf_ctx* ctx, const tf_heads* heads, int32_t stream_begin, in
  * embeddings [n][D] fp32 (used as given, like Detection.embedding),
  * has_embedding [n] (0 -> DimensionError if the detection survives NMS).
  * Device pointers. */
+/* Batched post-decode entry (the detection-file source, tf/detgen.py:366-484,
+ * fed through parse_output + Tracker.step, tf/pipeline.py:291-302): S streams x
+ * B frames (stream-major) of already-decoded rows. Frame f's rows are
+ * [row_offsets[f], row_offsets[f+1]) (HOST array of F + 1) of the DEVICE arrays
+ * boxes [N][4] tlwh, objectness [N] and embeddings [N][D] fp32. With
+ * normalized = 0 the embeddings are raw row values and are normalised here as
+ * parse_output does (DegenerateEmbeddingError on any row); with 1 they are
+ * parse_output's unit vectors already (e.g. rows whose raw values are not fp32,
+ * normalised by tf_normalize_rows from fp64). Records are written like
+ * tf_update_heads'. Asynchronous on `cuda_stream`. */
+int tf_update_detections(tf_ctx* ctx, int32_t stream_begin, int32_t n_streams, int32_t B,
+                         const int64_t* frame_index, const int32_t* row_offsets, const double* boxes,
+                         const double* objectness, const float* embeddings, int32_t normalized,
+                         const tf_records* out, const tf_trace* trace, void* cuda_stream);
+
 int tf_step_detections(tf_ctx* ctx, int32_t stream, int64_t frame_index, int32_t n,
                        const double* boxes, const double* objectness, const float* embeddings,
                        const uint8_t* has_embedding, const tf_records* out, const tf_trace* trace,

@@ -23,5 +23,6 @@ from .assoc import Assignment, apply_gate, build_cost_matrix, hungarian_solve, m
 from .tracker import STrack, Track, Tracker, TrackerConfig, TrackerOutput, TrackState, smooth_embedding  # noqa: F401
 from .engine import Capacity  # noqa: F401
 from .heads import BatchTracker, HeadOutputs, OnlineTracks  # noqa: F401
+from . import detfile  # noqa: F401  (detection-file source)
 
 __version__ = "0.1.0"

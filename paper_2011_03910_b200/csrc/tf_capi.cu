@@ -30,6 +30,7 @@ struct tf_ctx {
   // per-frame detection buffers
   DetBuf det;                 // = dets[0] (per-frame detection buffers)
   long long* d_frame_index;   // = d_fidx[0]
+  int* d_row_offsets;         // [max_frames + 1] row ranges of tf_update_detections
   // pipelining (tf_set_pipeline): two buffer sets, decode on the caller's
   // stream, association + outputs on `side`
   DetBuf dets[2];
@@ -316,6 +317,7 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
     A(&c->dets[b].code, F * Km);
     A(&c->dets[b].emb, F * Km * D);
     A(&c->d_fidx[b], F);
+    if (b == 0) A(&c->d_row_offsets, F + 1);
   }
   A(&c->trk.id, S * Tm);
   A(&c->trk.state, S * Tm);
@@ -607,6 +609,77 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     c->last_frame[stream_begin + ls] = frame_index[static_cast<size_t>(ls) * B + B - 1];
   c->last_begin = stream_begin;
   c->last_count = n_streams;
+  return TF_OK;
+}
+
+int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int32_t B, const int64_t* frame_index,
+                         const int32_t* row_offsets, const double* boxes, const double* objectness,
+                         const float* embeddings, int32_t normalized, const tf_records* out, const tf_trace* trace,
+                         void* cuda_stream) {
+  if (!c || !frame_index || !row_offsets || !out) return fail(c, TF_ARGUMENT, "null argument");
+  if (n_streams < 1 || B < 1 || stream_begin < 0 || stream_begin + n_streams > c->cap.streams)
+    return fail(c, TF_ARGUMENT, "stream range out of bounds");
+  const int F = n_streams * B;
+  if (F > c->cap.max_frames) return fail(c, TF_CAPACITY, "frames per update exceed max_frames");
+  if (out->max_records < 1) return fail(c, TF_ARGUMENT, "max_records must be >= 1");
+  if (row_offsets[0] != 0) return fail(c, TF_ARGUMENT, "row_offsets[0] must be 0");
+  for (int f = 0; f < F; ++f) {
+    const int n = row_offsets[f + 1] - row_offsets[f];
+    if (n < 0) return fail(c, TF_ARGUMENT, "row_offsets must be non-decreasing");
+    if (n > c->cap.max_candidates) return fail(c, TF_CAPACITY, "too many detections for max_candidates");
+  }
+  if (row_offsets[F] > 0 && (!boxes || !objectness || !embeddings)) return fail(c, TF_ARGUMENT, "null detection arrays");
+  int rc = check_step_config(c);
+  if (rc) return rc;
+  for (int ls = 0; ls < n_streams; ++ls) {
+    rc = check_ordering(c, stream_begin + ls, reinterpret_cast<const long long*>(frame_index) + static_cast<size_t>(ls) * B, B);
+    if (rc) return rc;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  TF_CUDA(c, cudaSetDevice(c->device));
+  for (int b = 0; b < 2; ++b)
+    if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
+  c->asc_pending[0] = c->asc_pending[1] = false;
+  TF_CUDA(c, upload_frame_index(c, c->d_frame_index, reinterpret_cast<const long long*>(frame_index), F, st));
+  TF_CUDA(c, cudaMemcpyAsync(c->d_row_offsets, row_offsets, sizeof(int32_t) * (F + 1), cudaMemcpyHostToDevice, st));
+  TF_CUDA(c, launch_frame_rows(boxes, objectness, embeddings, c->d_row_offsets, F, normalized ? 0 : 1,
+                               c->cap.max_candidates, c->cap.max_detections, c->det, c->P, st));
+  AssocArgs a;
+  a.det = c->det;
+  a.trk = c->trk;
+  a.trace = to_trace(trace);
+  a.frame_index = c->d_frame_index;
+  a.stream_begin = stream_begin;
+  a.B = B;
+  a.cap_tracks = c->cap.max_tracks;
+  a.cap_det = c->cap.max_detections;
+  a.cap_entries = c->cap_entries;
+  a.pool_col = c->pool_col;
+  a.pool_row = c->pool_row;
+  a.pool_val = c->pool_val;
+  a.pool_aux = c->pool_aux;
+  a.stats = c->profiling ? c->d_stats : nullptr;
+  {
+    const char* env = getenv("TF_CLUSTER");
+    const int key = n_streams * 64 + (env ? atoi(env) & 63 : 0);
+    if (key != c->cluster_key) {
+      c->cluster_val = assoc_cluster_size(n_streams, a.cap_tracks, a.cap_det, a.cap_entries);
+      c->cluster_key = key;
+    }
+    a.cluster = c->cluster_val;
+  }
+  a.out.count = out->count;
+  a.out.track_id = reinterpret_cast<long long*>(out->track_id);
+  a.out.box = out->box;
+  a.out.objectness = out->objectness;
+  a.out.max_records = out->max_records;
+  TF_CUDA(c, launch_associate(a, n_streams, c->P, st));
+  if (trace && trace->det_code)
+    copy_codes_kernel<<<F, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, F, c->cap.max_detections);
+  c->touched_lo = std::min(c->touched_lo, stream_begin);
+  c->touched_hi = std::max(c->touched_hi, stream_begin + n_streams);
+  for (int ls = 0; ls < n_streams; ++ls)
+    c->last_frame[stream_begin + ls] = frame_index[static_cast<size_t>(ls) * B + B - 1];
   return TF_OK;
 }
 

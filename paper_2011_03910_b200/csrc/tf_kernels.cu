@@ -414,17 +414,30 @@ struct RowsArgs {
   const double* boxes;
   const double* obj;
   const float* emb;
-  const uint8_t* has_emb;
+  const uint8_t* has_emb;          // null: every row has an embedding
+  const int* offsets;              // [frames + 1] row ranges (batched entry), or null: one frame of n rows
   int n, cap_cand, cap_det, words;
+  int normalize;                   // 1: rows are raw parse_output input (normalise, tf/postproc.py:31-33)
   DetBuf det;
 };
 
+// One CTA per frame: filter_confidence + NMS + detection buffer for rows that
+// are already decoded (Tracker.step, or the batched detection-file source).
 __global__ void __launch_bounds__(512) frame_dets_kernel(RowsArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, wid = warp_id(), nw = n_warps(), lane = lane_id();
   __shared__ int s_warp[33];
   __shared__ int s_misc[4];
-  const int f = 0;
+  const int f = blockIdx.x;
+  const int r0 = a.offsets ? a.offsets[f] : 0;
+  const int C_all = a.offsets ? a.offsets[f + 1] - r0 : a.n;
+  const int C = min(C_all, a.cap_cand);
+  const double* boxes = a.boxes + 4LL * r0;
+  const double* obj = a.obj + r0;
+  const uint8_t* has = a.has_emb ? a.has_emb + r0 : nullptr;
+  const int D = P.dim;
+  const float* emb = a.emb + static_cast<long long>(r0) * D;
+  const long long fb = static_cast<long long>(f) * a.cap_det;
   const FramePlan plan = frame_plan(0, a.cap_cand, a.words);
   double* cbox = reinterpret_cast<double*>(smem + plan.off_box);
   double* cscore = reinterpret_cast<double*>(smem + plan.off_score);
@@ -433,12 +446,14 @@ __global__ void __launch_bounds__(512) frame_dets_kernel(RowsArgs a, Params P) {
   unsigned long long* nmask = reinterpret_cast<unsigned long long*>(smem + plan.off_nmask);
   uint8_t* ckeep = smem + plan.off_keep;
   int16_t* cpos = reinterpret_cast<int16_t*>(smem + plan.off_pos);
-  if (tid == 0) s_misc[0] = STATUS_CLEAR;
-  const int C = a.n;
+  if (tid == 0) {
+    s_misc[0] = STATUS_CLEAR;
+    if (C_all > a.cap_cand) flag_error(&s_misc[0], 0, TF_CAPACITY);
+  }
   for (int r = tid; r < C; r += blockDim.x) {
-    for (int q = 0; q < 4; ++q) cbox[4 * r + q] = a.boxes[4 * r + q];
-    cscore[r] = a.obj[r];
-    calive[r] = a.obj[r] >= P.conf_threshold;
+    for (int q = 0; q < 4; ++q) cbox[4 * r + q] = boxes[4 * r + q];
+    cscore[r] = obj[r];
+    calive[r] = obj[r] >= P.conf_threshold;
   }
   __syncthreads();
   block_nms(C, cbox, cscore, calive, P.nms_iou, csorted, nmask, a.words, ckeep, &s_misc[1]);
@@ -448,26 +463,33 @@ __global__ void __launch_bounds__(512) frame_dets_kernel(RowsArgs a, Params P) {
   for (int r = tid; r < C; r += blockDim.x) {
     int k = cpos[r];
     if (k < 0 || k >= K) continue;
-    if (!a.has_emb[r]) flag_error(&s_misc[0], r + 1, TF_DIMENSION);
+    if (has && !has[r]) flag_error(&s_misc[0], r + 1, TF_DIMENSION);
     double m[4];
     box_to_meas(&cbox[4 * r], m);
-    double* dm = a.det.meas + static_cast<long long>(k) * 4;
+    double* dm = a.det.meas + (fb + k) * 4;
     dm[0] = m[0]; dm[1] = m[1]; dm[2] = m[2]; dm[3] = m[3];
-    a.det.obj[k] = cscore[r];
-    a.det.code[k] = r;
+    a.det.obj[fb + k] = cscore[r];
+    a.det.code[fb + k] = r;
   }
-  const int D = P.dim;
   for (int r = wid; r < C; r += nw) {
     int k = cpos[r];
-    if (k < 0 || k >= K || !a.has_emb[r]) continue;
-    const float* src = a.emb + static_cast<long long>(r) * D;
-    float* dst = a.det.emb + static_cast<long long>(k) * D;
+    const bool kept = k >= 0 && k < K;
+    if (a.normalize) {
+      // parse_output normalises every row (and raises on any degenerate one)
+      const int stn = gather_normalize<float>(emb + static_cast<long long>(r) * D, 1, D, P.quantize,
+                                              kept ? a.det.emb + (fb + k) * D : nullptr);
+      if (stn != TF_OK && lane == 0) flag_error(&s_misc[0], r + 1, stn);
+      continue;
+    }
+    if (!kept || (has && !has[r])) continue;
+    const float* src = emb + static_cast<long long>(r) * D;
+    float* dst = a.det.emb + (fb + k) * D;
     for (int i = lane; i < D; i += 32) dst[i] = src[i];
   }
   __syncthreads();
   if (tid == 0) {
     a.det.count[f] = K;
-    a.det.cand_count[f] = C;
+    a.det.cand_count[f] = C_all;
     int st = s_misc[0];
     a.det.status[f] = (st == STATUS_CLEAR) ? 0 : (st & 0xff);
   }
@@ -2290,7 +2312,9 @@ cudaError_t launch_frame_dets(const double* boxes, const double* obj, const floa
   a.obj = obj;
   a.emb = emb;
   a.has_emb = has;
+  a.offsets = nullptr;
   a.n = n;
+  a.normalize = 0;
   a.cap_cand = cap_cand;
   a.cap_det = cap_det;
   a.words = (cap_cand + 63) / 64;
@@ -2298,6 +2322,27 @@ cudaError_t launch_frame_dets(const double* boxes, const double* obj, const floa
   const size_t smem = frame_smem_bytes(0, cap_cand);
   cudaFuncSetAttribute(frame_dets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   frame_dets_kernel<<<1, 512, smem, st>>>(a, P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frame_rows(const double* boxes, const double* obj, const float* emb, const int* offsets,
+                              int frames, int normalize, int cap_cand, int cap_det, const DetBuf& det,
+                              const Params& P, cudaStream_t st) {
+  RowsArgs a;
+  a.boxes = boxes;
+  a.obj = obj;
+  a.emb = emb;
+  a.has_emb = nullptr;
+  a.offsets = offsets;
+  a.n = 0;
+  a.normalize = normalize;
+  a.cap_cand = cap_cand;
+  a.cap_det = cap_det;
+  a.words = (cap_cand + 63) / 64;
+  a.det = det;
+  const size_t smem = frame_smem_bytes(0, cap_cand);
+  cudaFuncSetAttribute(frame_dets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  frame_dets_kernel<<<frames, 512, smem, st>>>(a, P);
   return cudaGetLastError();
 }
 

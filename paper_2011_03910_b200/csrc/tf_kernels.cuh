@@ -87,6 +87,11 @@ size_t assoc_smem_bytes(int cap_tracks, int cap_det, int cap_entries);
 cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_t st);
 cudaError_t launch_frame_dets(const double* boxes, const double* obj, const float* emb, const uint8_t* has, int n,
                               int cap_cand, int cap_det, const DetBuf& det, const Params& P, cudaStream_t st);
+// Batched already-decoded rows (detection-file source): one CTA per frame,
+// rows of frame f at [offsets[f], offsets[f+1]), parse_output normalisation.
+cudaError_t launch_frame_rows(const double* boxes, const double* obj, const float* emb, const int* offsets,
+                              int frames, int normalize, int cap_cand, int cap_det, const DetBuf& det,
+                              const Params& P, cudaStream_t st);
 cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st);
 int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entries);
 cudaError_t launch_nms_sets(int n_sets, const int* offsets, const double* boxes, const double* scores,

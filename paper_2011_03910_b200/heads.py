@@ -24,6 +24,8 @@ from .engine import Capacity, Engine
 from .errors import LayoutError
 from .tracker import TrackerConfig, records_from_device
 
+ROW_WIDTH = 6   # parse_output row prefix: tlwh, objectness, class score (tf/postproc.py:16)
+
 INPUT_W, INPUT_H = 1088, 608
 IMAGE_W, IMAGE_H = 1920, 1080
 STRIDES = (32, 16, 8)
@@ -193,6 +195,64 @@ class BatchTracker:
         if host:
             return OnlineTracks(host_out["count"], host_out["track_id"], host_out["box"], host_out["objectness"],
                                 frames, B)
+        return OnlineTracks(eng.rec_count[:F], eng.rec_id[:F], eng.rec_box[:F], eng.rec_obj[:F], frames, B)
+
+    def update_rows(self, rows, frame_index=None, *, stream_begin: int = 0, n_streams: int | None = None,
+                    trace: bool = False, sync: bool = True) -> OnlineTracks:
+        """Post-decode entry: ``rows[f]`` is frame f's ``[n, 6 + D]`` parse_output
+        input (tlwh, objectness, class score, raw embedding; tf/postproc.py:19-42),
+        frames stream-major. Replays detector output (the detection-file source,
+        tf/detgen.py:366-484) through NMS and association in one launch per
+        update instead of one ``Tracker.step`` per frame."""
+        torch = self.engine.torch
+        eng = self.engine
+        n_streams = self.S if n_streams is None else n_streams
+        F = len(rows)
+        if F == 0 or F % n_streams:
+            raise LayoutError(f"{F} frames do not split over {n_streams} streams")
+        B = F // n_streams
+        D = self.config.embedding_dim
+        arrs = []
+        for f, r in enumerate(rows):
+            r = np.asarray(r, dtype=np.float64)
+            if r.size == 0:
+                r = np.zeros((0, ROW_WIDTH + D), np.float64)
+            if r.ndim != 2 or r.shape[1] != ROW_WIDTH + D:
+                raise LayoutError(f"frame {f}: expected rows of width {ROW_WIDTH + D}, got shape {r.shape}")
+            arrs.append(r)
+        offsets = np.zeros(F + 1, np.int32)
+        offsets[1:] = np.cumsum([a.shape[0] for a in arrs])
+        allr = np.concatenate(arrs) if offsets[-1] else np.zeros((0, ROW_WIDTH + D), np.float64)
+        boxes = np.ascontiguousarray(allr[:, :4])
+        # parse_output builds a BoundingBox per row (tf/core.py:37-43)
+        bad = ~(np.isfinite(boxes).all(axis=1) & (boxes[:, 2] > 0) & (boxes[:, 3] > 0))
+        if bad.any():
+            i = int(np.nonzero(bad)[0][0])
+            from .core import BoundingBox
+            BoundingBox(*(float(v) for v in boxes[i]))      # raises the reference's InvalidBoxError
+        emb64 = allr[:, ROW_WIDTH:]
+        emb32 = emb64.astype(np.float32)
+        normalized = 0
+        if not np.array_equal(emb32.astype(np.float64), emb64):
+            # raw values beyond fp32: parse_output's fp64 normalisation first (GPU)
+            from .core import normalize_rows
+            emb32 = normalize_rows(emb64)
+            normalized = 1
+        dev = eng.device
+        db = torch.as_tensor(boxes).to(dev)
+        do = torch.as_tensor(np.ascontiguousarray(allr[:, 4])).to(dev)
+        de = torch.as_tensor(np.ascontiguousarray(emb32)).to(dev)
+        frames = self._frames(n_streams, B, frame_index)
+        code = eng.lib.tf_update_detections(eng.ctx, stream_begin, n_streams, B, frames.ctypes.data,
+                                            offsets.ctypes.data, db.data_ptr() if allr.shape[0] else None,
+                                            do.data_ptr() if allr.shape[0] else None,
+                                            de.data_ptr() if allr.shape[0] else None, normalized,
+                                            C.byref(eng.records), C.byref(eng.trace) if trace else None,
+                                            _lib.stream_handle())
+        eng.check(code, "update_rows")
+        if sync:
+            eng.finish()
+        self.frame[stream_begin:stream_begin + n_streams] = frames.reshape(n_streams, B)[:, -1]
         return OnlineTracks(eng.rec_count[:F], eng.rec_id[:F], eng.rec_box[:F], eng.rec_obj[:F], frames, B)
 
     def host_output(self, frames: int) -> dict:
