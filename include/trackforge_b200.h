@@ -280,6 +280,30 @@ int tf_smooth_embedding(int32_t n, int32_t dim, const float* old_emb, const floa
 /* iou (tf/core.py:71-80) of n box pairs. */
 int tf_iou_pairs(int32_t n, const double* a, const double* b, double* out, void* cuda_stream);
 
+/* ---- MOT evaluation of tracker outputs (tf/moteval.py) ----
+ * All pointers DEVICE. Frames are the sorted union of gt and hypothesis frames;
+ * rows of frame f are [gt_ptr[f], gt_ptr[f+1]) (resp. hyp_ptr), ids are dense
+ * indices (< n_gt_ids / n_hyp_ids, unique within a frame), boxes tlwh fp64.
+ *
+ * tf_mot_accumulate = match_frame over every frame with the carried id mapping
+ * (accumulate, tf/moteval.py:36-110): match i of frame f is stored at index
+ * gt_ptr[f] + i (gt row, hyp row, IoU) in reference order (carried pairs in gt
+ * order, then hungarian_solve pairs by row); gt_matched / hyp_matched flag the
+ * rows. One CTA runs the frames in order; status[0] = TF_CAPACITY when a frame
+ * exceeds max_gt / max_hyp / max_pairs (pairs with IoU >= iou_min). */
+int tf_mot_accumulate(int32_t n_frames, const int32_t* gt_ptr, const int32_t* gt_id, const double* gt_box,
+                      const int32_t* hyp_ptr, const int32_t* hyp_id, const double* hyp_box, int32_t n_gt_ids,
+                      int32_t n_hyp_ids, int32_t max_gt_per_frame, int32_t max_hyp_per_frame,
+                      int32_t max_pairs_per_frame, double iou_min, int32_t* match_count, int32_t* match_gt,
+                      int32_t* match_hyp, double* match_iou, uint8_t* gt_matched, uint8_t* hyp_matched,
+                      int32_t* status, void* cuda_stream);
+/* Joint coverage of trajectory pairs for id_metrics (tf/moteval.py:196-232,
+ * 337-345): coverage[gt id][hyp id] (zero-initialised by the caller, int32,
+ * row-major n_gt_ids x n_hyp_ids) += frames where both are present with IoU >= iou_min. */
+int tf_mot_coverage(int32_t n_frames, const int32_t* gt_ptr, const int32_t* gt_id, const double* gt_box,
+                    const int32_t* hyp_ptr, const int32_t* hyp_id, const double* hyp_box, int32_t n_hyp_ids,
+                    double iou_min, int32_t* coverage, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

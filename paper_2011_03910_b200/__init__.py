@@ -24,5 +24,6 @@ from .tracker import STrack, Track, Tracker, TrackerConfig, TrackerOutput, Track
 from .engine import Capacity  # noqa: F401
 from .heads import BatchTracker, HeadOutputs, OnlineTracks  # noqa: F401
 from . import detfile  # noqa: F401  (detection-file source)
+from . import moteval  # noqa: F401  (MOT rows and metrics of GPU outputs)
 
 __version__ = "0.1.0"

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtrackforge_b200.so"
-SOURCES = ["tf_kernels.cu", "tf_capi.cu"]
+SOURCES = ["tf_kernels.cu", "tf_capi.cu", "tf_moteval.cu"]
 HEADERS = ["tf_device.cuh", "tf_kernels.cuh"]
 
 NVCC_FLAGS = [

@@ -113,4 +113,15 @@ cudaError_t launch_smooth(int n, int dim, const float* o, const float* q, double
                           int* status, cudaStream_t st);
 cudaError_t launch_iou(int n, const double* a, const double* b, double* out, cudaStream_t st);
 
+// MOT evaluation (tf_moteval.cu)
+size_t mot_accumulate_smem(int cap_g, int cap_h, int cap_e);
+cudaError_t launch_mot_accumulate(int frames, const int* gt_ptr, const int* gt_id, const double* gt_box,
+                                  const int* hyp_ptr, const int* hyp_id, const double* hyp_box, int n_gt_ids,
+                                  int n_hyp_ids, double iou_min, int cap_g, int cap_h, int cap_e, int* prev, int* hpos,
+                                  int* match_count, int* match_gt, int* match_hyp, double* match_iou,
+                                  uint8_t* gt_matched, uint8_t* hyp_matched, int* status, cudaStream_t st);
+cudaError_t launch_mot_coverage(int frames, const int* gt_ptr, const int* gt_id, const double* gt_box,
+                                const int* hyp_ptr, const int* hyp_id, const double* hyp_box, double iou_min,
+                                int n_hyp_ids, int* coverage, cudaStream_t st);
+
 }  // namespace tfd
