@@ -236,6 +236,30 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------- our arm
+def tracking_quality(args, cfg_name, S, B, cap, dev, steps=8):
+    """MOTA / IDF1 of the GPU outputs of stream 0 against the generator's
+    ground truth, scored by the GPU moteval; a fresh,
+    untimed run of `steps` updates with its own seed."""
+    import paper_2011_03910_b200 as p
+    from paper_2011_03910_b200 import moteval, synth
+    from paper_2011_03910_b200.tracker import TrackerOutput
+
+    gen = synth.make(cfg_name, device=dev, seed=args.seed + 1000, streams=S)
+    gen.record_truth()
+    bt = p.BatchTracker(S, frames_per_update=B, capacity=cap)
+    outs = []
+    for i in range(steps):
+        batch = gen.next_batch(B)
+        if args.dtype == "f16":
+            batch = batch.half()
+        r = bt.update(batch)
+        outs += [TrackerOutput(frame_index=int(r.frame_index[b]), records=r.records(0, b)) for b in range(B)]
+        del batch
+    rep = moteval.evaluate(gen.truth_frames(0), moteval.outputs_to_frames(outs))
+    return {"stream": 0, "frames": len(outs), "iou_min": 0.5, "MOTA": rep.mota, "IDF1": rep.idf1,
+            "MOTP": rep.motp, "IDs": rep.id_switches, "FP": rep.fp, "FN": rep.fn, "scorer": "GPU moteval"}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -403,6 +427,9 @@ def run_ours(args):
         tfile = ROOT / "profiles" / "traffic.json"
         if tfile.exists():
             traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dominant)
+        quality = None
+        if not streamed:
+            quality = tracking_quality(args, args.config, S, B, cap, dev)
         cpu = None
         if not args.no_cpu:
             if not multi:
@@ -466,6 +493,7 @@ def run_ours(args):
             "ranks": per_rank,
             "gpu_launches": 2 * K * (1 if not streamed else 1) + (K if streamed else 0),
             "clocks": clocks.summary(),
+            "quality": quality,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

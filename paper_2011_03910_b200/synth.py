@@ -87,6 +87,7 @@ class HeadSynth:
         self.r = 1.0 / self.scale_inv
         self.frame = 0
         self.next_identity = 1
+        self.truth = None          # list of per-frame ground truth once record_truth() was called
         shape = (S, hi)
         self.cx = torch.zeros(shape, dtype=torch.float64, device=self.device)
         self.cy = torch.zeros_like(self.cx)
@@ -139,7 +140,28 @@ class HeadSynth:
             out = (self.cx < 0) | (self.cx >= IMAGE_W) | (self.cy < 0) | (self.cy >= IMAGE_H)
             if bool(out.any()):
                 self._respawn(out)
+        if self.truth is not None:
+            w = self.h * self.cfg.aspect
+            box = torch.stack([self.cx - w / 2.0, self.cy - self.h / 2.0, w, self.h], dim=-1)
+            self.truth.append((self.frame, self.active.clone(), self.gid.clone(), box))
         self.frame += 1
+
+    def record_truth(self) -> None:
+        """Keep the ground truth of every frame generated from now on: all
+        active objects (occlusion dropouts included -- the detector misses them,
+        the scene still holds them), image-space tlwh, identity ids."""
+        self.truth = []
+
+    def truth_frames(self, stream: int = 0) -> dict:
+        """Ground truth of one stream as moteval frame boxes {frame: [(id, BoundingBox)]}."""
+        from .core import BoundingBox
+        out = {}
+        for frame, active, gid, box in self.truth or []:
+            sel = active[stream]
+            ids = gid[stream][sel].tolist()
+            bx = box[stream][sel].tolist()
+            out[frame] = [(int(i), BoundingBox(*b)) for i, b in zip(ids, bx)]
+        return out
 
     def alloc(self, frames: int):
         """Empty head / embedding tensors for ``frames`` frames (embeddings channels_last)."""
