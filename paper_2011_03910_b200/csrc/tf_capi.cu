@@ -296,9 +296,11 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   // keep as many gated entries on chip as the budget allows (the rest spill to a global pool)
   int entries = 8192;
-  while (entries > 64 && assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + 2048 > static_cast<size_t>(smem_optin))
+  const size_t assoc_static = assoc_static_smem() + 256;
+  while (entries > 64 &&
+         assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + assoc_static > static_cast<size_t>(smem_optin))
     entries -= 128;
-  if (assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + 2048 > static_cast<size_t>(smem_optin) ||
+  if (assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + assoc_static > static_cast<size_t>(smem_optin) ||
       frame_smem_bytes(54264, k.max_candidates) + 2048 > static_cast<size_t>(smem_optin)) {
     delete c;
     return TF_ARGUMENT;

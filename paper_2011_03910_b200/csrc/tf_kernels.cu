@@ -1259,8 +1259,12 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         int* cdn = cur ? c_nr : c_nc;
         int* rdn = cur ? c_ne : c_root;
         int16_t* lst = cur ? c_epos : c_elist;
-        for (int e0 = 0; e0 < E; e0 += blockDim.x) {
-          const int e = e0 + tid;
+        // rounds after the first walk only the previous round's live edges
+        const int16_t* src = round == 0 ? nullptr : (cur ? c_elist : c_epos);
+        const int n_src = round == 0 ? E : s_nlive[cur ^ 1];
+        for (int e0 = 0; e0 < n_src; e0 += blockDim.x) {
+          const int q = e0 + tid;
+          const int e = q < n_src ? (src ? static_cast<int>(src[q]) : q) : E;
           bool live = false;
           if (e < E) {
             const int r = erow[e], c = ecol[e];
@@ -1282,13 +1286,13 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
           if (live) lst[base + __popc(bm & ((1u << lane) - 1u))] = static_cast<int16_t>(e);
         }
         __syncthreads();
-        for (int e = tid; e < E; e += blockDim.x) {
+        const int n_cur = s_nlive[cur];
+        for (int q = tid; q < n_cur; q += blockDim.x) {      // this round's live edges
+          const int e = lst[q];
           const int r = erow[e], c = ecol[e];
-          if (p_ra[r] && p_ca[c]) {
-            const unsigned key = static_cast<unsigned>(__double_as_longlong(eval[e]) >> 32);
-            if (key == km[c]) atomicAdd(&cc[c], 1);
-            if (key == rk[r]) atomicAdd(&rc[r], 1);
-          }
+          const unsigned key = static_cast<unsigned>(__double_as_longlong(eval[e]) >> 32);
+          if (key == km[c]) atomicAdd(&cc[c], 1);
+          if (key == rk[r]) atomicAdd(&rc[r], 1);
         }
         __syncthreads();
         int* flag = cur ? &s_flag2 : &s_flag;
@@ -1405,7 +1409,11 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
             c_off[i] = isz - vsz;
             c_eoff[i] = ine - vne;
           }
-          if (lane == 0) { s_tie = tie; s_nmulti = n_multi; }
+          if (lane == 0) {
+            s_tie = tie;
+            s_nmulti = n_multi;
+            if (a.stats) s_ph[10] += n_multi;
+          }
         }
         __syncthreads();
       } else {
@@ -1475,7 +1483,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         const bool laid_out = n_multi >= 0;
         if (!laid_out) {
         n_multi = block_rank(NN, [&](int x) { return c_lab[x] == x && c_ne[x] >= 1; }, c_pos, s_warp);
-        if (a.stats && tid == 0) s_ph[10] += n_multi;
+        if (a.stats && tid == 0) s_ph[10] += n_multi;   // (the one-warp layout counts its own)
         for (int x = tid; x < NN; x += blockDim.x)
           if (c_pos[x] >= 0) c_root[c_pos[x]] = x;
         __syncthreads();
@@ -1513,6 +1521,25 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         }
         for (int i = wid; i < n_multi; i += nw) {
           const int root = c_root[i], off = c_off[i];
+          if (c_nr[root] == 1 || c_nc[root] == 1) {
+            // a star (one track wanting several detections, or one detection
+            // wanted by several tracks): the maximum matching has one pair and,
+            // with no equal costs in the component, the cheapest edge is it
+            double best = INFINITY;
+            int be = -1;
+            for (int q = lane; q < E_live; q += 32) {
+              const int e = c_elist[q];
+              if (c_lab[erow[e]] == root && eval[e] < best) { best = eval[e]; be = e; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const double ob = __shfl_xor_sync(FULL, best, o);
+              const int oe = __shfl_xor_sync(FULL, be, o);
+              if (ob < best || (ob == best && oe > be)) { best = ob; be = oe; }
+            }
+            if (lane == 0 && be >= 0) rcol[erow[be]] = ecol[be];
+            continue;
+          }
           int nr_l = 0, nc_l = 0;
           for (int t0 = 0; t0 < T; t0 += 32) {
             const int t = t0 + lane;
@@ -2255,6 +2282,12 @@ __global__ void iou_kernel(int n, const double* a, const double* b, double* out)
 size_t frame_smem_bytes(int total_anchors, int cap_cand) {
   return frame_plan(total_anchors, cap_cand, (cap_cand + 63) / 64).total;
 }
+size_t assoc_static_smem() {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, associate_kernel) != cudaSuccess) return 8192;
+  return fa.sharedSizeBytes;
+}
+
 size_t assoc_smem_bytes(int cap_tracks, int cap_det, int cap_entries) {
   return assoc_plan(cap_tracks, cap_det, cap_entries).total;
 }

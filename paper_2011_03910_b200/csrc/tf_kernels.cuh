@@ -82,6 +82,8 @@ struct HeadLaunch {
 };
 
 size_t frame_smem_bytes(int total_anchors, int cap_cand);
+// static shared memory of associate_kernel (budgeted next to the dynamic plan)
+size_t assoc_static_smem();
 size_t assoc_smem_bytes(int cap_tracks, int cap_det, int cap_entries);
 
 cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_t st);
