@@ -511,7 +511,7 @@ struct AssocPlan {
       off_ecol, off_erow, off_eval, off_u, off_v, off_dist, off_crow, off_path, off_r4c, off_c4r, off_rem,
       off_vr, off_vc, off_lab, off_cnr, off_cnc, off_cne, off_croot, off_coff, off_cpos, off_crows, off_ccols,
       off_cmap, off_rcol, off_rmap, off_lrp, off_eoff, off_il, off_epos, off_elist, off_pcmin, off_prmin, off_pccnt, off_pcdeg, off_pcrow, off_prdeg, off_prcnt, off_prc1,
-      off_pra, off_pca, off_pkr, off_pkc, off_emas, total;
+      off_pra, off_pca, off_pkr, off_pkc, off_emas, off_fstk, total;
 };
 
 __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
@@ -541,6 +541,7 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
   TF_TAKE(off_drow, 4 * K)
   TF_TAKE(off_dpos, 2 * K)
   TF_TAKE(off_emas, 4 * K)        // EMA work list of the frame (det -> pool slot), read by followers
+  TF_TAKE(off_fstk, 4 * T)        // free embedding-slot stack of the stream (kept on chip for the launch)
   TF_TAKE(off_ecol, 2 * E)
   TF_TAKE(off_erow, 2 * E)
   TF_TAKE(off_eval, 8 * E)
@@ -857,6 +858,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work, s_Efr, s_emaK, s_cmd;
   __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2, s_nlive[2], s_nmulti;   // the follower-applied EMA of frame s_ema_b
   int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
+  int* f_stk = reinterpret_cast<int*>(smem + pl.off_fstk);
 
   // optional phase timing (tf_set_profiling): cycles per phase + counters
   __shared__ long long s_ph[32];
@@ -971,6 +973,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     for (int q = 0; q < 8; ++q) t_mean[8 * t + q] = tb.mean[(sT + t) * 8 + q];
     for (int q = 0; q < 12; ++q) t_cov[12 * t + q] = tb.cov[(sT + t) * 12 + q];
   }
+  for (int i = tid; i < s_nfree; i += blockDim.x) f_stk[i] = tb.free_stack[sT + i];
   // frame table of the update (index, decode status, detection count) and
   // the first frame's detections: the per-frame scalar loads and the
   // measurement copy leave the frame's critical path
@@ -1763,7 +1766,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
             a.out.objectness[fR + r] = d_obj[k];
           }
         }
-        if (t_flag[t]) a.trk.free_stack[sT + base_free + rpos[t]] = t_slot[t];
+        if (t_flag[t]) f_stk[base_free + rpos[t]] = t_slot[t];
         mv = t_flag[t] == 0 && npos[t] != t;
         if (mv) {
           d = npos[t];
@@ -1806,7 +1809,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
           t_hits[t] = 1;
           t_lost[t] = -1;
           t_last[t] = frame;
-          slot = a.trk.free_stack[sT + nf - 1 - r];          // pop in birth order
+          slot = f_stk[nf - 1 - r];                           // pop in birth order
           t_slot[t] = slot;
           if (a.trace.det_track) {
             a.trace.det_track[fK + k] = next + r;
@@ -1866,6 +1869,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   }
   // ---- write the stream's state back -----------------------------------------
   T = s_T;
+  for (int i = tid; i < s_nfree; i += blockDim.x) tb.free_stack[sT + i] = f_stk[i];
   for (int t = tid; t < T; t += blockDim.x) {
     tb.id[sT + t] = t_id[t];
     tb.lost[sT + t] = t_lost[t];
