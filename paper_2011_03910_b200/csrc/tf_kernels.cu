@@ -2008,119 +2008,159 @@ __device__ void mm8(const double* A, const double* B, double* C, bool bt) {
     }
 }
 
-__global__ void kalman_kernel(int op, int n, Params P, const double* mean_in, const double* cov_in,
-                              const double* zin, double* mean_out, double* cov_out, int* status) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double m[8], c[64], z[4];
-  if (op != 0) {
-    for (int q = 0; q < 8; ++q) m[q] = mean_in[8 * i + q];
-    for (int q = 0; q < 64; ++q) c[q] = cov_in[64 * i + q];
-  }
-  if (op == 0 || op == 3)
-    for (int q = 0; q < 4; ++q) z[q] = zin[4 * i + q];
-  int st = 0;
-  if (op == 0) {
-    double h = z[3];
-    if (!(h > 0.0)) st = TF_INVALID_MEASUREMENT;
-    double mm[8], cc[12];
-    KF::initiate(P, z, mm, cc);
-    for (int q = 0; q < 8; ++q) mean_out[8 * i + q] = mm[q];
-    for (int q = 0; q < 64; ++q) cov_out[64 * i + q] = 0.0;
-    for (int a4 = 0; a4 < 4; ++a4) {
-      cov_out[64 * i + 9 * a4] = cc[3 * a4];
-      cov_out[64 * i + 9 * (a4 + 4)] = cc[3 * a4 + 2];
-    }
-  } else if (op == 1) {
-    const double h = m[3];
-    double F[64] = {0}, FP[64], R[64];
-    for (int q = 0; q < 8; ++q) F[9 * q] = 1.0;
-    for (int q = 0; q < 4; ++q) F[8 * q + q + 4] = 1.0;
-    double mo[8];
-    for (int r = 0; r < 8; ++r) {
-      double acc = 0.0;
-      for (int k = 0; k < 8; ++k) acc = acc + F[8 * r + k] * m[k];
-      mo[r] = acc;
-    }
-    mm8(F, c, FP, false);
-    mm8(FP, F, R, true);
-    for (int q = 0; q < 4; ++q) {
-      double sp = KF::qpos(P, q, h), sv = KF::qvel(P, q, h);
-      R[9 * q] = R[9 * q] + sp * sp;
-      R[9 * (q + 4)] = R[9 * (q + 4)] + sv * sv;
-    }
-    for (int r = 0; r < 8; ++r) {
-      mean_out[8 * i + r] = mo[r];
-      for (int k = 0; k < 8; ++k) cov_out[64 * i + 8 * r + k] = (R[8 * r + k] + R[8 * k + r]) / 2.0;
-    }
-  } else if (op == 2 || op == 3) {
-    const double h = m[3];
-    double S[16], Lc[16] = {0};
-    for (int r = 0; r < 4; ++r)
-      for (int k = 0; k < 4; ++k) S[4 * r + k] = c[8 * r + k];
-    for (int q = 0; q < 4; ++q) {
-      double rs = KF::rstd(P, q, h);
-      S[5 * q] = S[5 * q] + rs * rs;
-    }
-    if (op == 2) {
-      for (int q = 0; q < 4; ++q) mean_out[4 * i + q] = m[q];
-      for (int q = 0; q < 16; ++q) cov_out[16 * i + q] = S[q];
-    } else {
-      // Cholesky (lower), diagonal reciprocal as LAPACK/OpenBLAS applies it
-      double inv[4];
-      for (int j = 0; j < 4 && !st; ++j) {
-        double acc = S[5 * j];
-        for (int k = 0; k < j; ++k) acc = acc - Lc[4 * j + k] * Lc[4 * j + k];
-        if (!(acc > 0.0)) { st = TF_NUMERIC; break; }
-        Lc[5 * j] = sqrt(acc);
-        inv[j] = 1.0 / Lc[5 * j];
-        for (int r = j + 1; r < 4; ++r) {
-          double v = S[4 * r + j];
-          for (int k = 0; k < j; ++k) v = v - Lc[4 * r + k] * Lc[4 * j + k];
-          Lc[4 * r + j] = v * inv[j];
-        }
+// The KalmanFilter batch API on dense 8x8 states. A 64-thread block stages
+// its 64 covariances (and the outputs) through shared memory with coalesced
+// 16-byte-per-thread copies (rows padded to 65 doubles against bank
+// conflicts); each thread then runs the reference's matrix expressions for
+// its state on its shared-memory rows, in the reference's operation order.
+constexpr int kKfBlock = 64, kKfPad = 65;
+__device__ __forceinline__ double kf_F(int r, int k) { return (k == r || (r < 4 && k == r + 4)) ? 1.0 : 0.0; }
+
+__global__ void __launch_bounds__(kKfBlock) kalman_kernel(int op, int n, Params P, const double* mean_in,
+                                                          const double* cov_in, const double* zin,
+                                                          double* mean_out, double* cov_out, int* status) {
+  extern __shared__ __align__(16) double kf_smem[];
+  double* TA = kf_smem;                               // [64][65] input covariance, then working rows
+  double* TB = kf_smem + kKfBlock * kKfPad;           // [64][65] scratch, then outputs
+  const int tid = threadIdx.x, i0 = blockIdx.x * kKfBlock, i = i0 + tid;
+  const int nb = min(kKfBlock, n - i0);
+  if (op != 0)
+    for (int x = tid; x < nb * 64; x += kKfBlock) TA[(x >> 6) * kKfPad + (x & 63)] = cov_in[64LL * i0 + x];
+  __syncthreads();
+  const int out_w = op == 2 ? 16 : 64;                // output covariance elements per state
+  double* c = TA + tid * kKfPad;
+  double* o = TB + tid * kKfPad;
+  if (i < n) {
+    double m[8], z[4];
+    if (op != 0)
+      for (int q = 0; q < 8; ++q) m[q] = mean_in[8LL * i + q];
+    if (op == 0 || op == 3)
+      for (int q = 0; q < 4; ++q) z[q] = zin[4LL * i + q];
+    int st = 0;
+    if (op == 0) {
+      double h = z[3];
+      if (!(h > 0.0)) st = TF_INVALID_MEASUREMENT;
+      double mm[8], cc[12];
+      KF::initiate(P, z, mm, cc);
+      for (int q = 0; q < 8; ++q) mean_out[8LL * i + q] = mm[q];
+      for (int q = 0; q < 64; ++q) o[q] = 0.0;
+      for (int a4 = 0; a4 < 4; ++a4) {
+        o[9 * a4] = cc[3 * a4];
+        o[9 * (a4 + 4)] = cc[3 * a4 + 2];
       }
-      if (!st) {
-        // gain^T = S^-1 (P H^T)^T via L then L^T solves, column by column
-        double G[32];   // [4][8]
-        for (int col = 0; col < 8; ++col) {
-          double y[4];
-          for (int r = 0; r < 4; ++r) {
-            double v = c[8 * col + r];        // (P H^T)^T [r][col] = P[col][r]
-            for (int k = 0; k < r; ++k) v = v - Lc[4 * r + k] * y[k];
-            y[r] = v * inv[r];
-          }
-          for (int r = 3; r >= 0; --r) {
-            double v = y[r];
-            for (int k = r + 1; k < 4; ++k) v = v - Lc[4 * k + r] * G[8 * k + col];
-            G[8 * r + col] = v * inv[r];
-          }
-        }
-        double inn[4];
-        for (int q = 0; q < 4; ++q) inn[q] = z[q] - m[q];
-        double KS[32], NC[64];
-        for (int r = 0; r < 8; ++r) {
-          double acc = 0.0;
-          for (int k = 0; k < 4; ++k) acc = acc + G[8 * k + r] * inn[k];
-          mean_out[8 * i + r] = m[r] + acc;
-          for (int k = 0; k < 4; ++k) {
-            double s2 = 0.0;
-            for (int q = 0; q < 4; ++q) s2 = s2 + G[8 * q + r] * S[4 * q + k];
-            KS[4 * r + k] = s2;
-          }
-        }
+    } else if (op == 1) {
+      const double h = m[3];
+      for (int r = 0; r < 8; ++r) {
+        double acc = 0.0;
+        for (int k = 0; k < 8; ++k) acc = acc + kf_F(r, k) * m[k];
+        mean_out[8LL * i + r] = acc;
+      }
+      // FP = F P (into o), R = FP F^T (into c). With finite inputs the zero
+      // terms of the dense products add exact zeros, so only the two nonzero
+      // terms are summed (same single rounding); otherwise the dense sums run
+      // as mm8 computes them (0 * inf = NaN must propagate like the reference's).
+      bool finite = true;
+      for (int q = 0; q < 64; ++q) finite = finite && isfinite(c[q]);
+      if (finite) {
         for (int r = 0; r < 8; ++r)
-          for (int k = 0; k < 8; ++k) {
+          for (int j = 0; j < 8; ++j) o[8 * r + j] = r < 4 ? c[8 * r + j] + c[8 * (r + 4) + j] : c[8 * r + j];
+        for (int r = 0; r < 8; ++r)
+          for (int j = 0; j < 8; ++j) c[8 * r + j] = j < 4 ? o[8 * r + j] + o[8 * r + j + 4] : o[8 * r + j];
+      } else {
+        for (int r = 0; r < 8; ++r)
+          for (int j = 0; j < 8; ++j) {
             double acc = 0.0;
-            for (int q = 0; q < 4; ++q) acc = acc + KS[4 * r + q] * G[8 * q + k];
-            NC[8 * r + k] = c[8 * r + k] - acc;
+            for (int k = 0; k < 8; ++k) acc = acc + kf_F(r, k) * c[8 * k + j];
+            o[8 * r + j] = acc;
           }
         for (int r = 0; r < 8; ++r)
-          for (int k = 0; k < 8; ++k) cov_out[64 * i + 8 * r + k] = (NC[8 * r + k] + NC[8 * k + r]) / 2.0;
+          for (int j = 0; j < 8; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < 8; ++k) acc = acc + o[8 * r + k] * kf_F(j, k);
+            c[8 * r + j] = acc;
+          }
+      }
+      for (int q = 0; q < 4; ++q) {
+        double sp = KF::qpos(P, q, h), sv = KF::qvel(P, q, h);
+        c[9 * q] = c[9 * q] + sp * sp;
+        c[9 * (q + 4)] = c[9 * (q + 4)] + sv * sv;
+      }
+      for (int r = 0; r < 8; ++r)
+        for (int k = 0; k < 8; ++k) o[8 * r + k] = (c[8 * r + k] + c[8 * k + r]) / 2.0;
+    } else {
+      const double h = m[3];
+      double S[16], Lc[16] = {0};
+      for (int r = 0; r < 4; ++r)
+        for (int k = 0; k < 4; ++k) S[4 * r + k] = c[8 * r + k];
+      for (int q = 0; q < 4; ++q) {
+        double rs = KF::rstd(P, q, h);
+        S[5 * q] = S[5 * q] + rs * rs;
+      }
+      if (op == 2) {
+        for (int q = 0; q < 4; ++q) mean_out[4LL * i + q] = m[q];
+        for (int q = 0; q < 16; ++q) o[q] = S[q];
+      } else {
+        // Cholesky (lower), diagonal reciprocal as LAPACK/OpenBLAS applies it
+        double inv[4];
+        for (int j = 0; j < 4 && !st; ++j) {
+          double acc = S[5 * j];
+          for (int k = 0; k < j; ++k) acc = acc - Lc[4 * j + k] * Lc[4 * j + k];
+          if (!(acc > 0.0)) { st = TF_NUMERIC; break; }
+          Lc[5 * j] = sqrt(acc);
+          inv[j] = 1.0 / Lc[5 * j];
+          for (int r = j + 1; r < 4; ++r) {
+            double v = S[4 * r + j];
+            for (int k = 0; k < j; ++k) v = v - Lc[4 * r + k] * Lc[4 * j + k];
+            Lc[4 * r + j] = v * inv[j];
+          }
+        }
+        if (!st) {
+          // gain^T = S^-1 (P H^T)^T via L then L^T solves, column by column (G in o[0..31])
+          double* G = o;   // [4][8]
+          for (int col = 0; col < 8; ++col) {
+            double y[4];
+            for (int r = 0; r < 4; ++r) {
+              double v = c[8 * col + r];        // (P H^T)^T [r][col] = P[col][r]
+              for (int k = 0; k < r; ++k) v = v - Lc[4 * r + k] * y[k];
+              y[r] = v * inv[r];
+            }
+            for (int r = 3; r >= 0; --r) {
+              double v = y[r];
+              for (int k = r + 1; k < 4; ++k) v = v - Lc[4 * k + r] * G[8 * k + col];
+              G[8 * r + col] = v * inv[r];
+            }
+          }
+          double inn[4];
+          for (int q = 0; q < 4; ++q) inn[q] = z[q] - m[q];
+          // NC = P - (G^T S) G, row by row in place of P (row r reads only P row r)
+          for (int r = 0; r < 8; ++r) {
+            double acc = 0.0;
+            for (int k = 0; k < 4; ++k) acc = acc + G[8 * k + r] * inn[k];
+            mean_out[8LL * i + r] = m[r] + acc;
+            double KS[4];
+            for (int k = 0; k < 4; ++k) {
+              double s2 = 0.0;
+              for (int q = 0; q < 4; ++q) s2 = s2 + G[8 * q + r] * S[4 * q + k];
+              KS[k] = s2;
+            }
+            for (int k = 0; k < 8; ++k) {
+              double a2 = 0.0;
+              for (int q = 0; q < 4; ++q) a2 = a2 + KS[q] * G[8 * q + k];
+              c[8 * r + k] = c[8 * r + k] - a2;
+            }
+          }
+          for (int r = 0; r < 8; ++r)
+            for (int k = 0; k < 8; ++k) o[8 * r + k] = (c[8 * r + k] + c[8 * k + r]) / 2.0;
+        }
       }
     }
+    status[i] = st;
   }
-  status[i] = st;
+  __syncthreads();
+  for (int x = tid; x < nb * out_w; x += kKfBlock) {
+    const int r = x / out_w, q = x - r * out_w;
+    cov_out[static_cast<long long>(i0) * out_w + x] = TB[r * kKfPad + q];
+  }
 }
 
 __global__ void gating_kernel(int nt, const double* means, const double* covs, int nm, const double* z,
@@ -2480,7 +2520,9 @@ cudaError_t launch_lap_dense(int n, const int* shapes, const long long* cost_off
 cudaError_t launch_kalman(int op, int n, const Params& P, const double* mi, const double* ci, const double* z,
                           double* mo, double* co, int* status, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  kalman_kernel<<<(n + 63) / 64, 64, 0, st>>>(op, n, P, mi, ci, z, mo, co, status);
+  const size_t smem = 2 * sizeof(double) * kKfBlock * kKfPad;
+  cudaFuncSetAttribute(kalman_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  kalman_kernel<<<(n + kKfBlock - 1) / kKfBlock, kKfBlock, smem, st>>>(op, n, P, mi, ci, z, mo, co, status);
   return cudaGetLastError();
 }
 
