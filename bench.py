@@ -388,13 +388,19 @@ def run_ours(args):
         bt2.engine.finish()
         barrier()
         e2e_ms = e_start.elapsed_time(e_end)
+        tl = np.zeros(6 * 64)
+        ntl = C.c_int32()
+        lib.tf_timeline(bt2.engine.ctx, tl.ctypes.data, 64, C.byref(ntl))
+        tl = tl[:6 * min(ntl.value, 64)].reshape(-1, 6)
         f2, a2, n2 = C.c_double(), C.c_double(), C.c_int64()
         lib.tf_kernel_times(bt2.engine.ctx, C.byref(f2), C.byref(a2), C.byref(n2))
         h2 = C.c_double()
         lib.tf_copy_times(bt2.engine.ctx, C.byref(h2))
         e2e_kernels = {"h2d_ms_per_step": h2.value / max(n2.value, 1),
                        "frame_heads_ms_per_launch": f2.value / max(n2.value, 1),
-                       "associate_ms_per_launch": a2.value / max(n2.value, 1), "launches": n2.value}
+                       "associate_ms_per_launch": a2.value / max(n2.value, 1), "launches": n2.value,
+                       "assoc_gap_ms_mean": float(np.mean(tl[1:, 2] - tl[:-1, 3])) if len(tl) > 1 else None,
+                       "timeline_ms": [[round(float(v), 3) for v in row] for row in tl[:4]]}
         lib.tf_set_profiling(bt2.engine.ctx, 0)
         del host_batches
     h2d = F * conf_bytes + (cand / K) * esz * (4 + D) + 8 * F

@@ -222,6 +222,10 @@ int tf_kernel_times(tf_ctx* ctx, double* frame_ms, double* assoc_ms, int64_t* up
 /* Host->device copy milliseconds (pinned-host updates) summed over the window
  * read by the last tf_kernel_times call. */
 int tf_copy_times(tf_ctx* ctx, double* h2d_ms);
+/* Per-update event timeline since profiling was enabled (diagnostics): for
+ * update u, out[6u..6u+5] = frame kernel start/end, association start/end,
+ * host-input copy start/end in ms from the first update's copy start. */
+int tf_timeline(tf_ctx* ctx, double* out, int32_t max_updates, int32_t* n_updates);
 /* Per-phase SM cycles of associate_kernel summed over streams since profiling
  * was enabled (synchronising; resets): [0] load+predict [1] gate [2] CSR
  * [3] cosine cost [4] LAP [5] matches [6] Kalman update + EMA [7] records,

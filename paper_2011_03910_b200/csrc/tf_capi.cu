@@ -59,10 +59,16 @@ struct tf_ctx {
   // device staging used when inputs / outputs are host memory
   float* stage_conf[2][3];
   size_t stage_conf_elems[2][3];
-  int* rec_count;
-  long long* rec_id;
-  double* rec_box;
-  double* rec_obj;
+  // device staging of host-output records, one set per pipeline parity; the
+  // device->host copies run on their own stream so the next association
+  // does not queue behind them
+  int* rec_count[2];
+  long long* rec_id[2];
+  double* rec_box[2];
+  double* rec_obj[2];
+  cudaStream_t d2h;
+  cudaEvent_t ev_d2h[2];
+  bool d2h_pending[2];
   int rec_capacity;
   // streams touched by the last update (for tf_finish)
   int last_begin, last_count;
@@ -262,7 +268,11 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   c->last_begin = 0;
   c->last_count = 0;
   c->rec_capacity = 0;
-  c->rec_count = nullptr;
+  for (int b = 0; b < 2; ++b) {
+    c->rec_count[b] = nullptr;
+    c->d2h_pending[b] = false;
+  }
+  c->d2h = nullptr;
   c->profiling = 0;
   c->events_used = 0;
   c->prof_bytes_frame = 0;
@@ -349,9 +359,11 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   c->det = c->dets[0];
   c->d_frame_index = c->d_fidx[0];
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking);
   for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
     e = cudaEventCreateWithFlags(&c->ev_dec[b], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_asc[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_d2h[b], cudaEventDisableTiming);
   }
   for (int r = 0; r < tf_ctx::kRing && e == cudaSuccess; ++r) {
     e = cudaHostAlloc(&c->h_fidx[r], sizeof(long long) * F, cudaHostAllocDefault);
@@ -384,6 +396,11 @@ int tf_destroy(tf_ctx* ctx) {
     }
     cudaStreamDestroy(ctx->side);
   }
+  if (ctx->d2h) {
+    cudaStreamSynchronize(ctx->d2h);
+    for (int b = 0; b < 2; ++b) cudaEventDestroy(ctx->ev_d2h[b]);
+    cudaStreamDestroy(ctx->d2h);
+  }
   for (int r = 0; r < tf_ctx::kRing; ++r)
     if (ctx->h_fidx[r]) {
       cudaEventSynchronize(ctx->ev_fidx[r]);
@@ -409,15 +426,17 @@ int tf_reset_stream(tf_ctx* c, int32_t stream, void* cuda_stream) {
 
 static int ensure_record_staging(tf_ctx* c, int frames, int max_records) {
   const int need = frames * max_records;
-  if (need <= c->rec_capacity && c->rec_count) return TF_OK;
+  if (need <= c->rec_capacity && c->rec_count[0]) return TF_OK;
   cudaError_t e = cudaSuccess;
   auto A = [&](auto** p, size_t n) {
     if (e == cudaSuccess) e = dev_alloc(c, p, n);
   };
-  A(&c->rec_count, static_cast<size_t>(c->cap.max_frames));
-  A(&c->rec_id, static_cast<size_t>(need));
-  A(&c->rec_box, static_cast<size_t>(need) * 4);
-  A(&c->rec_obj, static_cast<size_t>(need));
+  for (int b = 0; b < 2; ++b) {
+    A(&c->rec_count[b], static_cast<size_t>(c->cap.max_frames));
+    A(&c->rec_id[b], static_cast<size_t>(need));
+    A(&c->rec_box[b], static_cast<size_t>(need) * 4);
+    A(&c->rec_obj[b], static_cast<size_t>(need));
+  }
   if (e != cudaSuccess) return fail(c, TF_CUDA, std::string("record staging: ") + cudaGetErrorString(e));
   c->rec_capacity = need;
   return TF_OK;
@@ -578,10 +597,12 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   if (host_out) {
     rc = ensure_record_staging(c, F, out->max_records);
     if (rc) return rc;
-    a.out.count = c->rec_count;
-    a.out.track_id = c->rec_id;
-    a.out.box = c->rec_box;
-    a.out.objectness = c->rec_obj;
+    a.out.count = c->rec_count[par];
+    a.out.track_id = c->rec_id[par];
+    a.out.box = c->rec_box[par];
+    a.out.objectness = c->rec_obj[par];
+    // the previous copy out of this staging set must have finished
+    if (c->d2h_pending[par]) TF_CUDA(c, cudaStreamWaitEvent(ast, c->ev_d2h[par], 0));
   } else {
     a.out.count = out->count;
     a.out.track_id = reinterpret_cast<long long*>(out->track_id);
@@ -600,10 +621,14 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     copy_codes_kernel<<<F, 128, 0, ast>>>(det.count, det.code, trace->det_code, F, c->cap.max_detections);
   if (host_out) {
     const size_t n = static_cast<size_t>(F) * out->max_records;
-    TF_CUDA(c, cudaMemcpyAsync(out->count, c->rec_count, sizeof(int) * F, cudaMemcpyDeviceToHost, ast));
-    TF_CUDA(c, cudaMemcpyAsync(out->track_id, c->rec_id, sizeof(long long) * n, cudaMemcpyDeviceToHost, ast));
-    TF_CUDA(c, cudaMemcpyAsync(out->box, c->rec_box, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, ast));
-    TF_CUDA(c, cudaMemcpyAsync(out->objectness, c->rec_obj, sizeof(double) * n, cudaMemcpyDeviceToHost, ast));
+    if (!c->pipeline) TF_CUDA(c, cudaEventRecord(c->ev_asc[par], ast));
+    TF_CUDA(c, cudaStreamWaitEvent(c->d2h, c->ev_asc[par], 0));
+    TF_CUDA(c, cudaMemcpyAsync(out->count, c->rec_count[par], sizeof(int) * F, cudaMemcpyDeviceToHost, c->d2h));
+    TF_CUDA(c, cudaMemcpyAsync(out->track_id, c->rec_id[par], sizeof(long long) * n, cudaMemcpyDeviceToHost, c->d2h));
+    TF_CUDA(c, cudaMemcpyAsync(out->box, c->rec_box[par], sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, c->d2h));
+    TF_CUDA(c, cudaMemcpyAsync(out->objectness, c->rec_obj[par], sizeof(double) * n, cudaMemcpyDeviceToHost, c->d2h));
+    TF_CUDA(c, cudaEventRecord(c->ev_d2h[par], c->d2h));
+    c->d2h_pending[par] = true;
   }
   c->touched_lo = std::min(c->touched_lo, stream_begin);
   c->touched_hi = std::max(c->touched_hi, stream_begin + n_streams);
@@ -741,7 +766,9 @@ int tf_finish(tf_ctx* c, void* cuda_stream) {
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   TF_CUDA(c, cudaStreamSynchronize(st));
   if (c->side) TF_CUDA(c, cudaStreamSynchronize(c->side));
+  if (c->d2h) TF_CUDA(c, cudaStreamSynchronize(c->d2h));
   c->asc_pending[0] = c->asc_pending[1] = false;
+  c->d2h_pending[0] = c->d2h_pending[1] = false;
   if (c->touched_hi <= c->touched_lo) return TF_OK;
   const int lo = c->touched_lo, n = c->touched_hi - c->touched_lo;
   c->touched_lo = 1 << 30;
@@ -762,7 +789,9 @@ int tf_finish(tf_ctx* c, void* cuda_stream) {
 int tf_set_pipeline(tf_ctx* c, int32_t enabled) {
   if (!c) return TF_ARGUMENT;
   if (c->side) TF_CUDA(c, cudaStreamSynchronize(c->side));
+  if (c->d2h) TF_CUDA(c, cudaStreamSynchronize(c->d2h));
   c->asc_pending[0] = c->asc_pending[1] = false;
+  c->d2h_pending[0] = c->d2h_pending[1] = false;
   c->pipeline = enabled ? 1 : 0;
   c->parity = 0;
   return TF_OK;
@@ -771,8 +800,10 @@ int tf_set_pipeline(tf_ctx* c, int32_t enabled) {
 int tf_join(tf_ctx* c, void* cuda_stream) {
   if (!c) return TF_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 2; ++b) {
     if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
+    if (c->d2h_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_d2h[b], 0));
+  }
   return TF_OK;
 }
 
@@ -831,6 +862,24 @@ int tf_phase_stats(tf_ctx* c, int64_t* out16) {
   TF_CUDA(c, cudaDeviceSynchronize());
   TF_CUDA(c, cudaMemcpy(out16, c->d_stats, 32 * sizeof(long long), cudaMemcpyDeviceToHost));
   TF_CUDA(c, cudaMemset(c->d_stats, 0, 32 * sizeof(long long)));
+  return TF_OK;
+}
+
+int tf_timeline(tf_ctx* c, double* out, int32_t max_updates, int32_t* n_updates) {
+  // per update: frame start/end, association start/end, copy start/end (ms
+  // from the first recorded event); call before tf_kernel_times (which resets)
+  if (!c || !out || !n_updates) return TF_ARGUMENT;
+  const int nu = static_cast<int>(c->events_used / 6);
+  *n_updates = nu;
+  if (nu == 0) return TF_OK;
+  TF_CUDA(c, cudaEventSynchronize(c->events[c->events_used - 3]));
+  const int order[6] = {0, 1, 2, 3, 4, 5};
+  for (int u = 0; u < nu && u < max_updates; ++u)
+    for (int k = 0; k < 6; ++k) {
+      float t = 0.f;
+      TF_CUDA(c, cudaEventElapsedTime(&t, c->events[4], c->events[6 * u + order[k]]));
+      out[6 * u + k] = t;
+    }
   return TF_OK;
 }
 
