@@ -1057,15 +1057,18 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       const int KC = (K + 31) >> 5;
       const double thr = P.gate_threshold;
       const bool maha = (P.gate_metric == 0);
-      for (int t0 = 4 * wid; t0 < T; t0 += 4 * nw) {
-        int cnt[4] = {0, 0, 0, 0};
+      constexpr int GU = 4;                // tracks per warp pass (independent fp64 chains; 2 and 8 measured slower)
+      for (int t0 = GU * wid; t0 < T; t0 += GU * nw) {
+        int cnt[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) cnt[u] = 0;
         for (int kc = 0; kc < KC; ++kc) {
           const int k = (kc << 5) + lane;
           const int kk = min(k, K - 1);
           const double z0 = d_meas[4 * kk], z1 = d_meas[4 * kk + 1], z2 = d_meas[4 * kk + 2], z3 = d_meas[4 * kk + 3];
-          double g[4];
+          double g[GU];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < GU; ++u) {
             const int t = min(t0 + u, T - 1);
             const double* m = &t_mean[8 * t];
             if (maha) {
@@ -1081,7 +1084,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
             }
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < GU; ++u) {
             const bool fin = k < K && t0 + u < T && !(g[u] > thr);
             const unsigned bm = __ballot_sync(FULL, fin);
             cnt[u] += __popc(bm);
@@ -1090,7 +1093,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         }
         if (lane == 0) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < GU; ++u)
             if (t0 + u < T) t_flag[t0 + u] = cnt[u];
         }
       }
@@ -1375,15 +1378,13 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
             if (!__any_sync(FULL, changed)) break;
           }
           if (on) root = c_lab[r];
-          // equal costs inside one component -> the exact full restatement
-          bool tie = false;
-          for (int j = 1; j < 32; ++j) {
-            const int src = (lane + j) & 31;
-            const double vo = __shfl_sync(FULL, v0, src);
-            const int ro = __shfl_sync(FULL, root, src);
-            tie = tie || (on && src < E_live && ro == root && vo == v0);
-          }
-          tie = __any_sync(FULL, tie);
+          // equal costs inside one component -> the exact full restatement:
+          // lanes with equal cost bits (zeros unified) that share a root
+          const unsigned long long vkey =
+              on ? (v0 == 0.0 ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v0))) : ~0ull - lane;
+          const unsigned same_v = __match_any_sync(FULL, vkey);
+          const unsigned same_r = __match_any_sync(FULL, on ? root : -1 - lane);
+          const bool tie = __any_sync(FULL, on && __popc(same_v & same_r) > 1);
           // distinct rows / columns / roots: the last writer of a marker owns it
           int* mark = c_lrp;
           if (on) { mark[r] = lane; mark[cn] = lane; }
