@@ -1,12 +1,20 @@
 """Group ncu source-page stall samples of associate_kernel by phase (line ranges of tf_kernels.cu)."""
 import csv, io, subprocess, sys
+from pathlib import Path
 from collections import defaultdict
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
-PH = [(1, 665, "prologue/helpers"), (666, 765, "setup"), (766, 818, "follower"), (819, 875, "load_predict"),
-      (876, 926, "gate"), (927, 970, "csr"), (971, 993, "cost"), (994, 1265, "lap"), (1266, 1286, "match"),
-      (1287, 1332, "update_ema"), (1333, 1459, "records"), (1460, 1490, "epilogue")]
+SRC = Path(__file__).resolve().parents[1] / "paper_2011_03910_b200" / "csrc" / "tf_kernels.cu"
+MARKERS = [("__device__ void cost_work", "cost_work(shared)"), ("__device__ void ema_work", "ema_work(shared)"),
+           ("associate_kernel(AssocArgs a", "setup"), ("  if (rank != 0) {", "follower"),
+           ("// ---- Kalman predict", "load_predict"), ("// ---- gate (", "gate"), ("// ---- CSR of finite", "csr"),
+           ("// ---- fp64 cosine cost", "cost"), ("// ---- exact LAP", "lap"), ("// ---- matches + max_cost", "match"),
+           ("// ---- matched: Kalman update", "update_ema"), ("// ---- records: matched", "records"),
+           ("// ---- release the follower", "epilogue"), ("__global__ void nms_sets_kernel", "stage kernels")]
+lines = SRC.read_text().splitlines()
+starts = sorted((next(i + 1 for i, l in enumerate(lines) if m in l), name) for m, name in MARKERS)
+PH = [(a, (starts[k + 1][0] - 1) if k + 1 < len(starts) else 10 ** 9, n) for k, (a, n) in enumerate(starts)]
 fname = None; hdr = None
 agg = defaultdict(lambda: defaultdict(int))
 for r in csv.reader(io.StringIO(out)):
@@ -17,9 +25,7 @@ for r in csv.reader(io.StringIO(out)):
     d = dict(zip(hdr[2:], r[2:]))
     ln = int(r[0])
     if fname == "tf_kernels.cu":
-        ph = next((n for a, b, n in PH if a <= ln <= b), "other")
-        if 518 <= ln <= 580: ph = "cost_work(shared)"
-        if 595 <= ln <= 658: ph = "ema_work(shared)"
+        ph = next((n for a, b, n in PH if a <= ln <= b), "frame/other")
     elif fname == "tf_device.cuh":
         ph = "dev:" + ("lap" if ln >= 300 else "KF/misc" if ln >= 95 else "util")
     else:
