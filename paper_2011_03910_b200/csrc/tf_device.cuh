@@ -57,6 +57,18 @@ __device__ __forceinline__ void flag_error(int* status, int position, int code) 
 }
 constexpr int STATUS_CLEAR = 0x7fffffff;
 
+// a / b in round-to-nearest from y = RN(1/b) (__drcp_rn): q0 = RN(a*y), the
+// remainder a - b*q0 is exact by FMA, and RN(q0 + rem*y) is the correctly
+// rounded quotient (Markstein's theorem; no overflow / underflow for the
+// unit-vector magnitudes it is used on). One reciprocal serves many
+// divisions by the same norm; tests/test_gpu_units.py checks it against
+// true division.
+__device__ __forceinline__ double div_by(double a, double b, double y) {
+  const double q0 = a * y;
+  const double r = fma(-b, q0, a);
+  return fma(r, y, q0);
+}
+
 // ---------------------------------------------------------------- geometry
 // iou, tf/core.py:71-80 (right = x + w, bottom = y + h, area = w * h; clamp to 1).
 __device__ __forceinline__ double iou_tlwh(double ax, double ay, double aw, double ah,

@@ -140,13 +140,14 @@ __device__ int gather_normalize(const T* src, long long stride, int dim, int qua
     if (out == nullptr) return TF_OK;
     if (vec) {
       float4* o4 = reinterpret_cast<float4*>(out);
+      const double rn = __drcp_rn(norm);
       for (int i = lane; i < dim / 4; i += 32) {
         float4 q = Elt<T>::ld4(src + 4 * i);
         float4 r;
-        r.x = static_cast<float>(static_cast<double>(q.x) / norm);
-        r.y = static_cast<float>(static_cast<double>(q.y) / norm);
-        r.z = static_cast<float>(static_cast<double>(q.z) / norm);
-        r.w = static_cast<float>(static_cast<double>(q.w) / norm);
+        r.x = static_cast<float>(div_by(static_cast<double>(q.x), norm, rn));
+        r.y = static_cast<float>(div_by(static_cast<double>(q.y), norm, rn));
+        r.z = static_cast<float>(div_by(static_cast<double>(q.z), norm, rn));
+        r.w = static_cast<float>(div_by(static_cast<double>(q.w), norm, rn));
         o4[i] = r;
       }
     } else {
@@ -740,13 +741,14 @@ __device__ void ema_work(const EmaView v) {
         continue;
       }
       float4* o4 = reinterpret_cast<float4*>(te);
+      const double rn = __drcp_rn(nrm);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         float4 r;
-        r.x = static_cast<float>(w[4 * q + 0] / nrm);
-        r.y = static_cast<float>(w[4 * q + 1] / nrm);
-        r.z = static_cast<float>(w[4 * q + 2] / nrm);
-        r.w = static_cast<float>(w[4 * q + 3] / nrm);
+        r.x = static_cast<float>(div_by(w[4 * q + 0], nrm, rn));
+        r.y = static_cast<float>(div_by(w[4 * q + 1], nrm, rn));
+        r.z = static_cast<float>(div_by(w[4 * q + 2], nrm, rn));
+        r.w = static_cast<float>(div_by(w[4 * q + 3], nrm, rn));
         o4[lane + 32 * q] = r;
       }
       continue;
