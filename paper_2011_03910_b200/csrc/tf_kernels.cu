@@ -185,7 +185,14 @@ __device__ int gather_normalize(const T* src, long long stride, int dim, int qua
 template <typename T, int kThreads>
 __global__ void __launch_bounds__(kThreads) frame_heads_kernel(FrameArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int f = blockIdx.x;
+  // With few frames a thread-block cluster scans each frame: every CTA takes a
+  // share of the anchor groups and stores its ballots into the leader CTA's
+  // shared memory (DSMEM); the leader then ranks, decodes, suppresses and
+  // gathers alone. One CTA per frame (cluster size 1) otherwise.
+  cg::cluster_group cl = cg::this_cluster();
+  const int CR = static_cast<int>(cl.num_blocks());
+  const int crank = static_cast<int>(cl.block_rank());
+  const int f = blockIdx.x / CR;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
 
   __shared__ const T* s_bg[12];
@@ -247,8 +254,10 @@ __global__ void __launch_bounds__(kThreads) frame_heads_kernel(FrameArgs a, Para
   const uint4* gmask_ro = reinterpret_cast<const uint4*>(smem + plan.off_masks);
   uint4* gmasks = reinterpret_cast<uint4*>(smem + plan.off_masks);
   const int NG = s_gstart[12];
-  const int per_warp = (NG + nw - 1) / nw;
-  const int g0 = min(NG, wid * per_warp), g1 = min(NG, g0 + per_warp);
+  const int nwc = nw * CR, gw = crank * nw + wid;            // the cluster's warps share the groups
+  const int per_warp = (NG + nwc - 1) / nwc;
+  const int g0 = min(NG, gw * per_warp), g1 = min(NG, g0 + per_warp);
+  uint4* out_masks = CR > 1 ? cl.map_shared_rank(gmasks, 0) : gmasks;
   const double lim = P.conf_logit;
   int count = 0;
   constexpr int U = 4;
@@ -287,10 +296,25 @@ __global__ void __launch_bounds__(kThreads) frame_heads_kernel(FrameArgs a, Para
         const unsigned m1 = __ballot_sync(FULL, (static_cast<double>(fgv[k].y) - static_cast<double>(bgv[k].y)) >= lim);
         const unsigned m2 = __ballot_sync(FULL, (static_cast<double>(fgv[k].z) - static_cast<double>(bgv[k].z)) >= lim);
         const unsigned m3 = __ballot_sync(FULL, (static_cast<double>(fgv[k].w) - static_cast<double>(bgv[k].w)) >= lim);
-        if (lane == 0) gmasks[g + k] = make_uint4(m0, m1, m2, m3);
+        if (lane == 0) out_masks[g + k] = make_uint4(m0, m1, m2, m3);
         count += __popc(m0) + __popc(m1) + __popc(m2) + __popc(m3);
       }
     }
+  }
+  // pass-2 ranges are the leader's own warps' over all groups
+  int p0 = g0, p1 = g1;
+  if (CR > 1) {
+    cl.sync();                                     // every CTA's ballots are in the leader
+    if (crank != 0) return;
+    const int pw = (NG + nw - 1) / nw;
+    p0 = min(NG, wid * pw);
+    p1 = min(NG, p0 + pw);
+    count = 0;
+    for (int gg = p0 + lane; gg < p1; gg += 32) {
+      const uint4 m = gmask_ro[gg];
+      count += __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
+    }
+    count = __reduce_add_sync(FULL, static_cast<unsigned>(count));
   }
   if (lane == 0) s_warp[wid] = count;
   __syncthreads();
@@ -314,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) frame_heads_kernel(FrameArgs a, Para
     int base = s_warp[wid];
     int pl = 0;
     const unsigned lt = (1u << lane) - 1u;
-    for (int gg = g0; gg < g1; ++gg) {
+    for (int gg = p0; gg < p1; ++gg) {
       const uint4 m = gmask_ro[gg];
       const int tot = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
       if (tot == 0) continue;
@@ -2382,9 +2406,28 @@ cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool many = h.frames >= 2 * sms;
+  int cr = 1;                                      // CTAs per frame (cluster) when frames are few
+  if (!many)
+    while (cr < 8 && h.frames * cr * 2 <= sms) cr *= 2;
   auto go = [&](auto kern, int threads) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kern<<<h.frames, threads, smem, st>>>(a, P);
+    if (cr == 1) {
+      kern<<<h.frames, threads, smem, st>>>(a, P);
+      return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(h.frames * cr));
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(cr);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a, P);
   };
   if (h.heads->dtype == 1) {          // binary16 heads and embedding maps
     if (many) go(frame_heads_kernel<__half, 256>, 256); else go(frame_heads_kernel<__half, 1024>, 1024);
