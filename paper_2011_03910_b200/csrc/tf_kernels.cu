@@ -15,12 +15,41 @@
 //                       binary16 / smooth / iou for the reference's module-level
 //                       functions.
 #include <cooperative_groups.h>
+#include <map>
+#include <mutex>
 
 #include "tf_kernels.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace tfd {
+
+// Host-side launch helpers: the dynamic shared-memory opt-in of a kernel is
+// only ever raised, once per size (cudaFuncSetAttribute costs microseconds
+// per call, which shows at small batches; every setter of these kernels goes
+// through here so the cache stays true), and the SM count is read once.
+static std::mutex g_attr_mu;
+static std::map<std::pair<const void*, int>, int> g_smem_set;     // (kernel, device) -> bytes set
+static void set_smem(const void* fn, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  const auto key = std::make_pair(fn, dev);
+  auto it = g_smem_set.find(key);
+  if (it != g_smem_set.end() && it->second >= static_cast<int>(bytes)) return;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)) == cudaSuccess)
+    g_smem_set[key] = static_cast<int>(bytes);
+}
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
 
 // ============================================================================
 // Frame stage (heads)
@@ -2402,15 +2431,13 @@ cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_
   int total = 0;
   for (int i = 0; i < 3; ++i) total += 4 * h.heads->scale[i].height * h.heads->scale[i].width;
   const size_t smem = frame_smem_bytes(total, h.cap_cand);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   const bool many = h.frames >= 2 * sms;
   int cr = 1;                                      // CTAs per frame (cluster) when frames are few
   if (!many)
     while (cr < 8 && h.frames * cr * 2 <= sms) cr *= 2;
   auto go = [&](auto kern, int threads) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    set_smem(reinterpret_cast<const void*>(kern), smem);
     if (cr == 1) {
       kern<<<h.frames, threads, smem, st>>>(a, P);
       return;
@@ -2453,7 +2480,7 @@ cudaError_t launch_frame_dets(const double* boxes, const double* obj, const floa
   a.words = (cap_cand + 63) / 64;
   a.det = det;
   const size_t smem = frame_smem_bytes(0, cap_cand);
-  cudaFuncSetAttribute(frame_dets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  set_smem(reinterpret_cast<const void*>(frame_dets_kernel), smem);
   frame_dets_kernel<<<1, 512, smem, st>>>(a, P);
   return cudaGetLastError();
 }
@@ -2474,14 +2501,14 @@ cudaError_t launch_frame_rows(const double* boxes, const double* obj, const floa
   a.words = (cap_cand + 63) / 64;
   a.det = det;
   const size_t smem = frame_smem_bytes(0, cap_cand);
-  cudaFuncSetAttribute(frame_dets_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  set_smem(reinterpret_cast<const void*>(frame_dets_kernel), smem);
   frame_dets_kernel<<<frames, 512, smem, st>>>(a, P);
   return cudaGetLastError();
 }
 
 cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st) {
   const size_t smem = assoc_smem_bytes(a.cap_tracks, a.cap_det, a.cap_entries);
-  cudaFuncSetAttribute(associate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  set_smem(reinterpret_cast<const void*>(associate_kernel), smem);
   if (a.cluster <= 1) {
     associate_kernel<<<n_streams, kAssocThreads, smem, st>>>(a, P);
     return cudaGetLastError();
@@ -2516,7 +2543,7 @@ int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entri
   while (c > 1 && n_streams * c > sms) c >>= 1;
   if (c > 1) {
     const size_t smem = assoc_smem_bytes(cap_tracks, cap_det, cap_entries);
-    cudaFuncSetAttribute(associate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    set_smem(reinterpret_cast<const void*>(associate_kernel), smem);   // (only ever raised: see set_smem)
     if (c > 8) cudaFuncSetAttribute(associate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(c));

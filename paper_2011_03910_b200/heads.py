@@ -141,6 +141,7 @@ class BatchTracker:
             raise ValueError("capacity.streams < num_streams")
         self.engine = Engine(self.config, cap, quantize=quantize)
         self.frame = np.full(self.S, -1, np.int64)
+        self._desc, self._desc_key, self._views = None, None, {}
         self.pipeline = bool(pipeline)
         if self.pipeline:
             self.engine.check(self.engine.lib.tf_set_pipeline(self.engine.ctx, 1), "pipeline")
@@ -176,7 +177,7 @@ class BatchTracker:
         if host and not all(t.is_pinned() for t in (*head_outputs.heads, *head_outputs.embs)):
             raise LayoutError("host inputs must be pinned (torch.Tensor.pin_memory())")
         frames = self._frames(n_streams, B, frame_index)
-        desc = heads_descriptor(head_outputs, host)
+        desc = self._descriptor(head_outputs, host)
         if host:
             if host_out is None:
                 host_out = self.host_output(F)
@@ -253,7 +254,25 @@ class BatchTracker:
         if sync:
             eng.finish()
         self.frame[stream_begin:stream_begin + n_streams] = frames.reshape(n_streams, B)[:, -1]
-        return OnlineTracks(eng.rec_count[:F], eng.rec_id[:F], eng.rec_box[:F], eng.rec_obj[:F], frames, B)
+        views = self._views.get(F)
+        if views is None:
+            views = self._views[F] = (eng.rec_count[:F], eng.rec_id[:F], eng.rec_box[:F], eng.rec_obj[:F])
+        return OnlineTracks(*views, frames, B)
+
+    def _descriptor(self, out: HeadOutputs, host: bool) -> _lib.TfHeads:
+        """heads_descriptor with the layout validated once per tensor layout:
+        later updates with the same shapes / strides / dtype only swap the data
+        pointers (the per-update host cost matters at small batches)."""
+        key = (host,) + tuple((t.shape, t.stride(), t.dtype) for t in (*out.heads, *out.embs))
+        if self._desc_key != key:
+            self._desc = heads_descriptor(out, host)
+            self._desc_key = key
+            return self._desc
+        d = self._desc
+        for i in range(3):
+            d.scale[i].head = out.heads[i].data_ptr()
+            d.scale[i].emb = out.embs[i].data_ptr()
+        return d
 
     def host_output(self, frames: int) -> dict:
         torch = self.engine.torch
