@@ -1243,6 +1243,8 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     TF_SUB(22);
     if (C > 1) cg::this_cluster().sync();                          // S2: costs written
     TF_SUB(23);
+    // the previous frame's EMA list was consumed before S1: reset it
+    for (int k = tid; k < K; k += blockDim.x) ema_slot[k] = -1;
     if (tid == 0) s_work = 0;
     if (wid == 0) {                       // amplitude of the finite costs (read by the LAP after barriers)
       double m = 0.0;
@@ -1688,12 +1690,15 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     __syncthreads();
     TF_SUB(19);
     TF_MARK(4);
-    // ---- matches + max_cost threshold (tf/assoc.py:77-107) -----------------
-    if (gating) {
-      for (int t = tid; t < T; t += blockDim.x) {
+    // ---- matches + max_cost threshold (tf/assoc.py:77-107), then the
+    // matched tracks' Kalman update + lifecycle (tf/tracker.py:114-143), one
+    // thread per track in one pass; matched tracks also post their EMA work
+    TF_MARK(5);
+    for (int t = tid; t < T; t += blockDim.x) {
+      int md = -1;
+      double mc = 0.0;
+      if (gating) {
         const int c = rcol[t];
-        int md = -1;
-        double mc = 0.0;
         if (c >= 0) {
           for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
             if (ecol[e] == c) {
@@ -1702,19 +1707,14 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
               break;
             }
         }
-        t_mdet[t] = md;
-        t_mcost[t] = mc;
-        if (md >= 0) d_row[md] = t;
       }
-    }
-    __syncthreads();
-    TF_MARK(5);
-    // ---- matched: Kalman update + lifecycle (tf/tracker.py:114-125) --------
-    for (int t = tid; t < T; t += blockDim.x) {
-      const int k = t_mdet[t];
+      t_mdet[t] = md;
+      t_mcost[t] = mc;
       int remove = 0;
-      if (k >= 0) {
-        if (!KF::update(P, &t_mean[8 * t], &t_cov[12 * t], &d_meas[4 * k]))
+      if (md >= 0) {
+        d_row[md] = t;
+        ema_slot[md] = t_slot[t];
+        if (!KF::update(P, &t_mean[8 * t], &t_cov[12 * t], &d_meas[4 * md]))
           flag_error(&s_err, t + 1, TF_NUMERIC);
         t_state[t] = 0;
         t_lost[t] = -1;
@@ -1730,7 +1730,6 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       t_flag[t] = remove;
     }
     }  // frame_ok
-    for (int k = tid; k < K; k += blockDim.x) ema_slot[k] = (frame_ok && d_row[k] >= 0) ? t_slot[d_row[k]] : -1;
     if (tid == 0) { s_emaK = frame_ok ? K : 0; s_ema_work = 0; if (frame_ok) s_ema_b = b; }
     __syncthreads();
     if (C > 1) {
