@@ -660,89 +660,129 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
 // The association of one stream is sequential per frame, but two of its phases
 // are embarrassingly parallel and L2-latency bound: the fp64 cosine costs of the
 // un-gated pairs and the EMA appearance updates. With a thread-block cluster per
-// stream, follower CTAs join exactly these phases: work is handed out through
-// an atomic counter in the leader's shared memory (DSMEM), and results are
-// written back into it. Views carry leader-local or DSMEM-mapped pointers.
+// stream, follower CTAs join exactly these phases. Costs are statically
+// partitioned over every warp of the cluster; a follower reads the entry list
+// through DSMEM and sends each cost back with an asynchronous remote store
+// that counts its bytes on a leader mbarrier (st.async ... complete_tx), so
+// the leader's wait ends when the last cost lands, without a release fence.
+
+// pairs per warp per round (one L2 round trip per frame where possible)
+__device__ __forceinline__ int cost_nb(int E, int n_workers) { return E > 2 * n_workers ? 4 : 2; }
+
+// entries of a frame costed by follower warps (workers >= lead_workers)
+__device__ __forceinline__ int follower_entries(int E, int n_workers, int lead_workers) {
+  const int NB = cost_nb(E, n_workers);
+  const int nblk = E / NB, rem = E - nblk * NB;
+  int lead = NB * ((nblk / n_workers) * lead_workers + min(nblk % n_workers, lead_workers));
+  if (rem && (nblk % n_workers) < lead_workers) lead += rem;
+  return E - lead;
+}
+
+__device__ __forceinline__ void st_async_f64(unsigned cluster_addr_, double v, unsigned cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(cluster_addr_),
+               "l"(__double_as_longlong(v)), "r"(cluster_bar)
+               : "memory");
+}
+
 struct CostView {
-  const int* rowptr;
   const int16_t* ecol;
   const int16_t* erow;
   double* eval;
   const int* t_slot;
-  int* work;
   double* ampw;                // per-worker max cost (one slot per cluster warp)
+  unsigned eval_cl, ampw_cl;   // leader addresses of eval / ampw for st.async ...
+  unsigned bar_cl;             // ... counted on this leader mbarrier (0: plain stores)
   const float* pool;           // this stream's embedding pool
   const float* dets;           // this frame's detection embeddings
-  int T, E, D;
+  int E, D;
 };
 
-__device__ void cost_work(const CostView v, int worker, int n_workers) {
-  // Entry pairs are statically partitioned over every warp of the cluster
-  // (worker = global warp index): no atomics on the critical path, and each
-  // warp keeps 2 x 2 KB x 2 rows of 128-bit loads in flight per pair.
+// NB entry pairs per warp per round: every row of a round is in flight at once.
+template <int NB>
+__device__ __forceinline__ double cost_rounds(const CostView v, int worker, int n_workers) {
   const int lane = lane_id();
   double amp = 0.0;
-  for (int e0 = 2 * worker; e0 < v.E; e0 += 2 * n_workers) {
-    const bool two = e0 + 1 < v.E;
-    const int e1 = two ? e0 + 1 : e0;
-    // remote (DSMEM) loads are issued per thread: lanes 0..3 fetch the indices,
-    // the slots follow, and shuffles broadcast them
+  for (int e0 = NB * worker; e0 < v.E; e0 += NB * n_workers) {
+    const int n = min(NB, v.E - e0);
+    // remote (DSMEM) loads are issued per thread: lanes 0..NB-1 fetch the
+    // detection indices, lanes NB..2NB-1 the pool slots; shuffles broadcast them
     int idx = 0;
-    if (lane < 4) idx = (lane & 1) ? ((lane & 2) ? v.ecol[e1] : v.erow[e1]) : ((lane & 2) ? v.ecol[e0] : v.erow[e0]);
-    int sl = 0;
-    if (lane == 0 || lane == 1) sl = v.t_slot[idx];
-    const int k0 = __shfl_sync(FULL, idx, 2), k1 = __shfl_sync(FULL, idx, 3);
-    const int sl0 = __shfl_sync(FULL, sl, 0), sl1 = __shfl_sync(FULL, sl, 1);
-    const float* te0 = v.pool + static_cast<long long>(sl0) * v.D;
-    const float* te1 = v.pool + static_cast<long long>(sl1) * v.D;
-    const float* de0 = v.dets + static_cast<long long>(k0) * v.D;
-    const float* de1 = v.dets + static_cast<long long>(k1) * v.D;
-    double acc0 = 0.0, acc1 = 0.0;
+    if (lane < 2 * NB) {
+      const int e = e0 + min(lane % NB, n - 1);
+      idx = lane < NB ? v.ecol[e] : v.erow[e];
+      if (lane >= NB) idx = v.t_slot[idx];
+    }
+    int k[NB], sl[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      k[j] = __shfl_sync(FULL, idx, j);
+      sl[j] = __shfl_sync(FULL, idx, NB + j);
+    }
+    double acc[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[j] = 0.0;
     if (v.D == 512) {
-      const float4 *x0 = reinterpret_cast<const float4*>(te0), *y0 = reinterpret_cast<const float4*>(de0);
-      const float4 *x1 = reinterpret_cast<const float4*>(te1), *y1 = reinterpret_cast<const float4*>(de1);
-      float4 a0[4], b0[4], a1[4], b1[4];
+      float4 a[NB][4], b[NB][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a0[q] = x0[lane + 32 * q];
-        b0[q] = y0[lane + 32 * q];
-        a1[q] = x1[lane + 32 * q];
-        b1[q] = y1[lane + 32 * q];
+      for (int j = 0; j < NB; ++j) {
+        const float4* x = reinterpret_cast<const float4*>(v.pool + static_cast<long long>(sl[j]) * 512);
+        const float4* y = reinterpret_cast<const float4*>(v.dets + static_cast<long long>(k[j]) * 512);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[j][q] = x[lane + 32 * q];
+          b[j][q] = y[lane + 32 * q];
+        }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc0 = fma(static_cast<double>(a0[q].x), static_cast<double>(b0[q].x), acc0);
-        acc1 = fma(static_cast<double>(a1[q].x), static_cast<double>(b1[q].x), acc1);
-        acc0 = fma(static_cast<double>(a0[q].y), static_cast<double>(b0[q].y), acc0);
-        acc1 = fma(static_cast<double>(a1[q].y), static_cast<double>(b1[q].y), acc1);
-        acc0 = fma(static_cast<double>(a0[q].z), static_cast<double>(b0[q].z), acc0);
-        acc1 = fma(static_cast<double>(a1[q].z), static_cast<double>(b1[q].z), acc1);
-        acc0 = fma(static_cast<double>(a0[q].w), static_cast<double>(b0[q].w), acc0);
-        acc1 = fma(static_cast<double>(a1[q].w), static_cast<double>(b1[q].w), acc1);
-      }
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          acc[j] = fma(static_cast<double>(a[j][q].x), static_cast<double>(b[j][q].x), acc[j]);
+          acc[j] = fma(static_cast<double>(a[j][q].y), static_cast<double>(b[j][q].y), acc[j]);
+          acc[j] = fma(static_cast<double>(a[j][q].z), static_cast<double>(b[j][q].z), acc[j]);
+          acc[j] = fma(static_cast<double>(a[j][q].w), static_cast<double>(b[j][q].w), acc[j]);
+        }
     } else {
-      for (int i = lane; i < v.D; i += 32) {
-        acc0 = fma(static_cast<double>(te0[i]), static_cast<double>(de0[i]), acc0);
-        acc1 = fma(static_cast<double>(te1[i]), static_cast<double>(de1[i]), acc1);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const float* te = v.pool + static_cast<long long>(sl[j]) * v.D;
+        const float* de = v.dets + static_cast<long long>(k[j]) * v.D;
+        for (int i = lane; i < v.D; i += 32) acc[j] = fma(static_cast<double>(te[i]), static_cast<double>(de[i]), acc[j]);
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      acc0 += __shfl_xor_sync(FULL, acc0, o);
-      acc1 += __shfl_xor_sync(FULL, acc1, o);
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] += __shfl_xor_sync(FULL, acc[j], o);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      if (j < n) {
+        const double c = fmin(fmax(1.0 - acc[j], 0.0), 2.0);
+        if (lane == 0) {
+          if (v.bar_cl) st_async_f64(v.eval_cl + 8u * static_cast<unsigned>(e0 + j), c, v.bar_cl);
+          else v.eval[e0 + j] = c;
+        }
+        amp = fmax(amp, c);
+      }
     }
-    const double c0 = fmin(fmax(1.0 - acc0, 0.0), 2.0);
-    const double c1 = fmin(fmax(1.0 - acc1, 0.0), 2.0);
-    if (lane == 0) {
-      v.eval[e0] = c0;
-      if (two) v.eval[e1] = c1;
-    }
-    amp = fmax(amp, c0);
-    if (two) amp = fmax(amp, c1);
   }
+  return amp;
+}
+
+// Kept out of line: the kernel runs at the register cap, and inlining this
+// phase's 2 x 4 rows of loads perturbs the allocation of every other phase.
+__device__ __noinline__ void cost_work(const CostView v, int worker, int n_workers) {
+  // Entry pairs are statically partitioned over every warp of the cluster
+  // (worker = global warp index): no atomics on the critical path. Up to
+  // 4 pairs per warp per round (4 x 2 rows x 2 KB of 128-bit loads in flight)
+  // so a frame's entries take one round trip to L2 where possible.
+  const double amp = cost_nb(v.E, n_workers) == 4 ? cost_rounds<4>(v, worker, n_workers) : cost_rounds<2>(v, worker, n_workers);
   // amplitude = max |finite| (tf/assoc.py:71): one slot per worker, reduced
   // by the leader (a contended u64 atomicMax over DSMEM is a CAS loop)
-  if (lane == 0) v.ampw[worker] = amp;
+  if (lane_id() == 0) {
+    if (v.bar_cl) st_async_f64(v.ampw_cl + 8u * static_cast<unsigned>(worker), amp, v.bar_cl);
+    else v.ampw[worker] = amp;
+  }
 }
 
 struct EmaView {
@@ -757,7 +797,12 @@ struct EmaView {
 
 // EMA appearance update (tf/tracker.py:67-71, 117-119): one warp per matched
 // detection, normalize(alpha * old + (1 - alpha) * new) in fp64, fp32 out.
-__device__ void ema_work(const EmaView v) {
+#ifdef TF_EMA_NOINLINE
+__device__ __noinline__
+#else
+__device__
+#endif
+void ema_work(const EmaView v) {
   const int lane = lane_id();
   for (;;) {
     int k = 0;
@@ -825,13 +870,49 @@ __device__ void ema_work(const EmaView v) {
   }
 }
 
-// Split cluster barrier (arrive now, wait later): the leader publishes a
-// frame's EMA list and runs on while the follower CTAs apply it.
+// Cluster hand-offs of a frame. Leader -> followers (entries ready, EMA list
+// published): the hardware cluster barrier, the leader arriving with release
+// semantics and waiting for the phase only before its next arrive; the
+// scalars a follower needs are pushed into its shared memory first.
+// Followers -> leader: costs arrive by st.async on a transaction-counting
+// mbarrier; the EMA of a frame, applied while the leader runs on, is
+// signalled by one release arrive per follower on another leader mbarrier.
 __device__ __forceinline__ void cluster_arrive_release() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void cluster_wait_acquire() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ unsigned cluster_addr(const void* p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void st_cluster(unsigned cluster_addr_, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(cluster_addr_), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "TF_MBAR_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra TF_MBAR_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a, Params P) {
@@ -914,7 +995,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
 
   __shared__ int s_warp[33];
   __shared__ unsigned long long s_scan64[33];
-  __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_work, s_Efr, s_emaK, s_cmd;
+  __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_Efr;
   __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2, s_nlive[2], s_nmulti;   // the follower-applied EMA of frame s_ema_b
   int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
   int* f_stk = reinterpret_cast<int*>(smem + pl.off_fstk);
@@ -950,51 +1031,63 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   int16_t* erow = smem_erow;
   double* eval = smem_eval;
 
+  // Leader mbarriers: [0] EMA applied (C - 1 follower release arrivals),
+  // [1] costs landed (leader arrive + expected st.async bytes), [2] costs
+  // written to the global pool (C - 1 follower release arrivals; frames
+  // whose entries overflow shared memory). The leader pushes the scalars a
+  // follower needs into its s_fl before each cluster-barrier release:
+  // {stop, E, T, K of the EMA list}.
+  __shared__ __align__(8) unsigned long long s_bar[3];
+  __shared__ __align__(16) int s_fl[4];
+  if (C > 1) {
+    if (tid == 0 && rank == 0) {
+      mbar_init(&s_bar[0], C - 1);
+      mbar_init(&s_bar[1], 1);
+      mbar_init(&s_bar[2], C - 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cg::this_cluster().sync();
+  }
+
   if (rank != 0) {
     // ---- follower CTA: joins the cost and EMA phases of every frame -------
     cg::cluster_group cl = cg::this_cluster();
-    const int* L_cmd = cl.map_shared_rank(&s_cmd, 0);
-    const int* L_T = cl.map_shared_rank(&s_T, 0);
-    const int* L_E = cl.map_shared_rank(&s_Efr, 0);
-    const int* L_K = cl.map_shared_rank(&s_emaK, 0);
+    const unsigned L_ema_done = cluster_addr(&s_bar[0], 0);
+    const unsigned L_cost_tx = cluster_addr(&s_bar[1], 0);
+    const unsigned L_cost_pool = cluster_addr(&s_bar[2], 0);
     const long long sTf = static_cast<long long>(s) * Tm;
     for (int b = 0;; ++b) {
-      cl.sync();                                                      // S1
-      // leader scalars: one remote load each, shared through local memory
-      __shared__ int s_fl[3];
-      if (tid == 0) { s_fl[0] = *L_cmd; s_fl[1] = *L_E; s_fl[2] = *L_T; }
-      __syncthreads();
-      if (s_fl[0]) {
-        cl.sync();
-        return;
-      }
+      cluster_arrive_relaxed();                                        // S1: entries ready
+      cluster_wait_acquire();
+      if (s_fl[0]) return;                                             // stop: nothing of ours is read any more
       const long long fKf = static_cast<long long>(ls * a.B + b) * Km;
       const int E = s_fl[1];
+      const bool pooled = E > a.cap_entries;
       if (E > 0) {
         CostView cv;
-        const bool pooled = E > a.cap_entries;
-        cv.rowptr = cl.map_shared_rank(rowptr, 0);
         cv.ecol = pooled ? a.pool_col + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(smem_ecol, 0);
         cv.erow = pooled ? a.pool_row + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(smem_erow, 0);
-        cv.eval = pooled ? a.pool_val + static_cast<long long>(s) * Tm * Km : cl.map_shared_rank(smem_eval, 0);
+        cv.eval = pooled ? a.pool_val + static_cast<long long>(s) * Tm * Km : nullptr;
         cv.t_slot = cl.map_shared_rank(t_slot, 0);
-        cv.work = cl.map_shared_rank(&s_work, 0);
         cv.ampw = cl.map_shared_rank(s_ampw, 0);
+        cv.eval_cl = cluster_addr(smem_eval, 0);
+        cv.ampw_cl = cluster_addr(s_ampw, 0);
+        cv.bar_cl = pooled ? 0u : L_cost_tx;
         cv.pool = a.trk.emb_pool + sTf * static_cast<long long>(D);
         cv.dets = a.det.emb + fKf * static_cast<long long>(D);
-        cv.T = s_fl[2];
         cv.E = E;
         cv.D = D;
         cost_work(cv, rank * n_warps() + warp_id(), n_warps() * C);
+        if (pooled) {                                                  // S2 (pooled): costs written
+          __syncthreads();
+          if (tid == 0) mbar_arrive_remote(L_cost_pool);
+        }
       }
-      cl.sync();                                                      // S2
-      cl.sync();                                                      // S3: EMA list published
-      __shared__ int s_fk;
-      if (tid == 0) s_fk = *L_K;
-      __syncthreads();
+      cluster_arrive_relaxed();                                        // S3: EMA list published
+      cluster_wait_acquire();
       // The EMA of frame b runs while the leader finishes frame b and starts
-      // frame b + 1; the next S1 orders it before that frame's costs.
-      const int Ke = s_fk;
+      // frame b + 1; the leader waits for it before releasing that frame's costs.
+      const int Ke = s_fl[3];
       if (Ke > 0) {
         EmaView ev;
         ev.slot = cl.map_shared_rank(ema_slot, 0);
@@ -1008,10 +1101,17 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
         ev.D = D;
         ema_work(ev);
       }
+      __syncthreads();
+      if (tid == 0) mbar_arrive_remote(L_ema_done);                    // EMA applied
     }
   }
-  if (tid == 0) { s_cmd = 0; s_ema_err = STATUS_CLEAR; s_ema_b = -1; s_emaK = 0; }
-  bool s3_pending = false;        // leader arrived at S3 and has not waited yet
+  if (tid == 0) { s_ema_err = STATUS_CLEAR; s_ema_b = -1; }
+  bool ema_out = false;           // followers may still be applying an EMA list
+  bool s3_pending = false;        // the leader arrived at S3 and has not waited for the phase
+  unsigned ph_ema_done = 0, ph_cost_tx = 0, ph_cost_pool = 0;
+  // lane j of warp 0 pushes follower j + 1's scalars
+  const bool signaller = C > 1 && wid == 0 && lane < C - 1;
+  const unsigned F_fl = signaller ? cluster_addr(s_fl, lane + 1) : 0u;
   TrackBuf& tb = a.trk;
   const long long sT = static_cast<long long>(s) * Tm;
   if (tid == 0) {
@@ -1078,7 +1178,7 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     }
     const int K = frame_count(b);
     T = s_T;
-    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; s_work = 0; s_Efr = 0; t_frame0 = clock64(); }
+    if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; s_Efr = 0; t_frame0 = clock64(); }
     // this frame's detections were prefetched (this thread's copies land here;
     // the predict barrier publishes all of them); start the next frame's
     d_meas = (b & 1) ? d_meas1 : d_meas0;
@@ -1218,34 +1318,54 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
     __syncthreads();
     // ---- fp64 cosine cost of un-gated pairs (tf/assoc.py:34-46), cluster-wide --
     if (C > 1) {
-      if (s3_pending) cluster_wait_acquire();                      // S3 of the previous frame
+      if (s3_pending) cluster_wait_acquire();                      // previous frame's S3 phase
       s3_pending = false;
-      cg::this_cluster().sync();                                   // S1: entries ready, previous EMA done
+      if (ema_out) {                                               // previous frame's EMA applied
+        mbar_wait(&s_bar[0], ph_ema_done);
+        ph_ema_done ^= 1u;
+        ema_out = false;
+      }
+      TF_SUB(24);
+      const int Ef = s_Efr;
+      if (signaller) {
+        st_cluster(F_fl, 0);
+        st_cluster(F_fl + 4, Ef);
+        st_cluster(F_fl + 8, T);
+      }
+      if (tid == 0 && Ef > 0 && Ef <= a.cap_entries)               // bytes the followers will send
+        mbar_arrive_expect_tx(&s_bar[1], 8u * static_cast<unsigned>(follower_entries(Ef, nw * C, nw) + (C - 1) * nw));
+      cluster_arrive_release();                                    // S1: entries ready
+      TF_SUB(25);
     }
     TF_SUB(21);
     if (gating) {
       CostView cv;
-      cv.rowptr = rowptr;
       cv.ecol = ecol;
       cv.erow = erow;
       cv.eval = eval;
       cv.t_slot = t_slot;
-      cv.work = &s_work;
       cv.ampw = s_ampw;
+      cv.eval_cl = cv.ampw_cl = cv.bar_cl = 0u;
       cv.pool = a.trk.emb_pool + sT * static_cast<long long>(D);
       cv.dets = a.det.emb + fK * static_cast<long long>(D);
-      cv.T = T;
       cv.E = s_Efr;
       cv.D = D;
       cost_work(cv, wid, nw * C);
     }
     __syncthreads();
     TF_SUB(22);
-    if (C > 1) cg::this_cluster().sync();                          // S2: costs written
+    if (C > 1 && s_Efr > 0) {                                      // S2: costs written
+      if (s_Efr <= a.cap_entries) {
+        mbar_wait(&s_bar[1], ph_cost_tx);
+        ph_cost_tx ^= 1u;
+      } else {
+        mbar_wait(&s_bar[2], ph_cost_pool);
+        ph_cost_pool ^= 1u;
+      }
+    }
     TF_SUB(23);
     // the previous frame's EMA list was consumed before S1: reset it
     for (int k = tid; k < K; k += blockDim.x) ema_slot[k] = -1;
-    if (tid == 0) s_work = 0;
     if (wid == 0) {                       // amplitude of the finite costs (read by the LAP after barriers)
       double m = 0.0;
       if (s_Efr > 0)
@@ -1730,11 +1850,16 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       t_flag[t] = remove;
     }
     }  // frame_ok
-    if (tid == 0) { s_emaK = frame_ok ? K : 0; s_ema_work = 0; if (frame_ok) s_ema_b = b; }
+    if (tid == 0) { s_ema_work = 0; if (frame_ok) s_ema_b = b; }
     __syncthreads();
     if (C > 1) {
+      TF_SUB(27);
+      if (signaller) st_cluster(F_fl + 12, frame_ok ? K : 0);
+      cluster_wait_acquire();                                     // this frame's S1 phase
       cluster_arrive_release();                                   // S3: EMA list published
+      TF_SUB(26);
       s3_pending = true;
+      ema_out = true;
     } else if (frame_ok) {
       EmaView ev;
       ev.slot = ema_slot;
@@ -1919,11 +2044,11 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
   __syncthreads();
   // ---- release the follower CTAs (they wait at the S1 barrier) ----------------
   if (C > 1) {
-    if (tid == 0) s_cmd = 1;
-    __syncthreads();
     if (s3_pending) cluster_wait_acquire();
-    cg::this_cluster().sync();        // S1': followers read the stop command (their last EMA is done)
-    cg::this_cluster().sync();        // followers are done with this CTA's memory
+    if (ema_out) mbar_wait(&s_bar[0], ph_ema_done);   // followers are done with this CTA's memory
+    if (signaller) st_cluster(F_fl, 1);               // stop
+    cluster_arrive_release();
+    cluster_wait_acquire();
     if (tid == 0 && s_status == 0 && s_ema_err != STATUS_CLEAR) s_status = (s_ema_b << 8) | (s_ema_err & 0xff);
   }
   // ---- write the stream's state back -----------------------------------------
