@@ -518,7 +518,7 @@ def main():
     ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--batch", type=int, default=None, help="frames per stream per update (default: config's B)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-host-gb", type=float, default=24.0)
     ap.add_argument("--cpu-frames", type=int, default=640)
     ap.add_argument("--cpu-stream-frames", type=int, default=40)
