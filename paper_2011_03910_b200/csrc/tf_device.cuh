@@ -679,12 +679,7 @@ __device__ inline void warp_lap_reg(int n, int nr, const Rows R, double sentinel
 
 // Exact solver dispatch: register-resident for n <= 256, shared-memory otherwise.
 template <class Rows>
-#ifdef TF_LAP_NOINLINE
-__device__ __noinline__
-#else
-__device__ inline
-#endif
-void warp_lap_fast(int n, int nr, const Rows R, double sentinel, LapScratch s, int n_proc = -1) {
+__device__ inline void warp_lap_fast(int n, int nr, const Rows R, double sentinel, LapScratch s, int n_proc = -1) {
   if (n_proc < 0) n_proc = n;
   if (n <= 32) warp_lap_reg<1>(n, nr, R, sentinel, s, n_proc);
   else if (n <= 64) warp_lap_reg<2>(n, nr, R, sentinel, s, n_proc);

@@ -797,12 +797,7 @@ struct EmaView {
 
 // EMA appearance update (tf/tracker.py:67-71, 117-119): one warp per matched
 // detection, normalize(alpha * old + (1 - alpha) * new) in fp64, fp32 out.
-#ifdef TF_EMA_NOINLINE
-__device__ __noinline__
-#else
-__device__
-#endif
-void ema_work(const EmaView v) {
+__device__ void ema_work(const EmaView v) {
   const int lane = lane_id();
   for (;;) {
     int k = 0;
