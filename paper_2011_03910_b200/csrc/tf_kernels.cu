@@ -656,6 +656,32 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
 }
 
 
+// Embedding rows of a frame's births, one warp per birth: each new track's
+// pool slot (popped in birth order) receives its detection's embedding. Out
+// of line so the row held in registers does not weigh on the kernel's
+// register allocation.
+__device__ __noinline__ void birth_rows(const float* dets, float* pool, const int16_t* d_pos, const int* f_stk, int nf,
+                                        int K, int D) {
+  const int lane = lane_id();
+  for (int k = warp_id(); k < K; k += n_warps()) {
+    const int r = d_pos[k];
+    if (r < 0) continue;
+    const float* src = dets + static_cast<long long>(k) * D;
+    float* dst = pool + static_cast<long long>(f_stk[nf - 1 - r]) * D;
+    if (D == 512) {
+      float4 x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = reinterpret_cast<const float4*>(src)[lane + 32 * q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) reinterpret_cast<float4*>(dst)[lane + 32 * q] = x[q];
+    } else if ((D & 3) == 0) {
+      for (int i = lane; i < D / 4; i += 32) reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
+    } else {
+      for (int i = lane; i < D; i += 32) dst[i] = src[i];
+    }
+  }
+}
+
 // ---- cluster-cooperative phases of associate_kernel ----------------------------
 // The association of one stream is sequential per frame, but two of its phases
 // are embarrassingly parallel and L2-latency bound: the fp64 cosine costs of the
@@ -1974,6 +2000,8 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
       const int nf = base_free + n_rm;
       const long long next = s_next;
       TF_MARK(7);
+      birth_rows(a.det.emb + fK * static_cast<long long>(D), a.trk.emb_pool + sT * static_cast<long long>(D), d_pos,
+                 f_stk, nf, K, D);
       for (int k = wid; k < K; k += nw) {   // (births + frame tail: slot 30)
         const int r = d_pos[k];
         if (r < 0) continue;
@@ -2005,15 +2033,6 @@ __global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a
               a.out.objectness[fR + rr] = d_obj[k];
             }
           }
-        }
-        slot = __shfl_sync(FULL, slot, 0);
-        float* dst = a.trk.emb_pool + (sT + slot) * static_cast<long long>(D);
-        const float* src = a.det.emb + (fK + k) * static_cast<long long>(D);
-        if ((D & 3) == 0) {
-          for (int i = lane; i < D / 4; i += 32)
-            reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
-        } else {
-          for (int i = lane; i < D; i += 32) dst[i] = src[i];
         }
       }
       if (tid == 0) {
