@@ -328,7 +328,9 @@ def run_ours(args):
                 recs += int(r.count.sum())
         del twin
 
-    lib.tf_set_profiling(eng.ctx, 1)
+    # kernel events in the timed region; the in-kernel phase timers (level 2)
+    # only in the separate diagnostic pass below (streamed runs keep them on)
+    lib.tf_set_profiling(eng.ctx, 2 if streamed else 1)
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ms = 0.0
     barrier()
@@ -362,6 +364,18 @@ def run_ours(args):
     phase = np.zeros(32, np.int64)
     lib.tf_phase_stats(eng.ctx, phase.ctypes.data)
     lib.tf_set_profiling(eng.ctx, 0)
+    if not streamed:
+        # per-phase breakdown of the association: the same batches on a fresh
+        # tracker with the phase timers on, outside the timed region
+        pbt = p.BatchTracker(S, frames_per_update=B, capacity=cap, pipeline=pipe)
+        lib.tf_set_profiling(pbt.engine.ctx, 2)
+        for i in range(W + K):
+            pbt.update(batches[i], trace=False, sync=False)
+        pbt.join()
+        pbt.engine.finish()
+        lib.tf_phase_stats(pbt.engine.ctx, phase.ctypes.data)
+        lib.tf_set_profiling(pbt.engine.ctx, 0)
+        del pbt
 
     # ---- end to end through the C ABI with pinned host buffers --------------
     e2e_steps = min(K, args.e2e_steps)

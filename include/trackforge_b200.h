@@ -214,14 +214,19 @@ int tf_join(tf_ctx* ctx, void* cuda_stream);
 int tf_export_tracks(tf_ctx* ctx, int32_t stream, tf_track_export* out, void* cuda_stream);
 
 /* Optional CUDA-event timing of the two kernels of every update (bench.py).
- * tf_kernel_times synchronises, returns the summed milliseconds of
- * frame_heads_kernel and associate_kernel over the updates since the last
- * call, and resets the accumulators. */
+ * enabled: 0 off, 1 kernel events, 2 kernel events + the association
+ * kernel's in-kernel phase timers (tf_phase_stats; they cost ~1% of the
+ * kernel, so timed runs use 1). tf_kernel_times synchronises, returns the
+ * summed milliseconds of frame_heads_kernel and associate_kernel over the
+ * updates since the last call, and resets the accumulators. */
 int tf_set_profiling(tf_ctx* ctx, int32_t enabled);
 int tf_kernel_times(tf_ctx* ctx, double* frame_ms, double* assoc_ms, int64_t* updates);
 /* Host->device copy milliseconds (pinned-host updates) summed over the window
  * read by the last tf_kernel_times call. */
 int tf_copy_times(tf_ctx* ctx, double* h2d_ms);
+/* Association launch shape (diagnostics): threads per CTA (256, or 128 with
+ * two CTAs per SM for many streams) and CTAs per stream of the last update. */
+int tf_launch_info(tf_ctx* ctx, int32_t* assoc_threads, int32_t* assoc_cluster);
 /* Per-update event timeline since profiling was enabled (diagnostics): for
  * update u, out[6u..6u+5] = frame kernel start/end, association start/end,
  * host-input copy start/end in ms from the first update's copy start. */

@@ -81,6 +81,7 @@ _SIGS = {
     "tf_set_profiling": (c_i32, [c_vp, c_i32]),
     "tf_kernel_times": (c_i32, [c_vp, C.POINTER(c_dbl), C.POINTER(c_dbl), C.POINTER(c_i64)]),
     "tf_copy_times": (c_i32, [c_vp, C.POINTER(c_dbl)]),
+    "tf_launch_info": (c_i32, [c_vp, C.POINTER(c_i32), C.POINTER(c_i32)]),
     "tf_timeline": (c_i32, [c_vp, c_vp, c_i32, C.POINTER(c_i32)]),
     "tf_mot_accumulate": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_dbl,
                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -27,6 +27,7 @@ struct tf_ctx {
   Params P;
   std::string err;
   int cap_entries;
+  int assoc_threads;              // 256, or 128 (two association CTAs per SM) for many streams
   // per-frame detection buffers
   DetBuf det;                 // = dets[0] (per-frame detection buffers)
   long long* d_frame_index;   // = d_fidx[0]
@@ -307,6 +308,22 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   // keep as many gated entries on chip as the budget allows (the rest spill to a global pool)
   int entries = 8192;
   const size_t assoc_static = assoc_static_smem() + 256;
+  int sms = 0, smem_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  // Many streams (>= 2 per SM): two 128-thread association CTAs per SM when
+  // the plan fits half of the SM's shared memory with >= 1024 on-chip entries
+  // (the association is latency-bound, so two streams per SM nearly double
+  // its throughput). Otherwise one 256-thread CTA (or a cluster) per stream.
+  const size_t half = static_cast<size_t>(smem_sm) / 2 - 1024;
+  c->assoc_threads = kAssocThreads;
+  // (TF_ASSOC_NARROW / TF_ASSOC_WIDE force the choice: tests and A/B runs)
+  if ((k.streams >= 2 * static_cast<size_t>(sms) || getenv("TF_ASSOC_NARROW")) && !getenv("TF_ASSOC_WIDE") &&
+      assoc_smem_bytes(k.max_tracks, k.max_detections, 1024) + assoc_static <= half) {
+    c->assoc_threads = kAssocThreadsSmall;
+    while (entries > 1024 && assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + assoc_static > half)
+      entries -= 128;
+  }
   while (entries > 64 &&
          assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + assoc_static > static_cast<size_t>(smem_optin))
     entries -= 128;
@@ -579,16 +596,17 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.cap_tracks = c->cap.max_tracks;
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
+  a.threads = c->assoc_threads;
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
-  a.stats = c->profiling ? c->d_stats : nullptr;
+  a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
   {
     const char* env = getenv("TF_CLUSTER");
     const int key = n_streams * 64 + (env ? atoi(env) & 63 : 0);
     if (key != c->cluster_key) {
-      c->cluster_val = assoc_cluster_size(n_streams, a.cap_tracks, a.cap_det, a.cap_entries);
+      c->cluster_val = a.threads == kAssocThreadsSmall ? 1 : assoc_cluster_size(n_streams, a.cap_tracks, a.cap_det, a.cap_entries);
       c->cluster_key = key;
     }
     a.cluster = c->cluster_val;
@@ -681,16 +699,17 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   a.cap_tracks = c->cap.max_tracks;
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
+  a.threads = c->assoc_threads;
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
-  a.stats = c->profiling ? c->d_stats : nullptr;
+  a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
   {
     const char* env = getenv("TF_CLUSTER");
     const int key = n_streams * 64 + (env ? atoi(env) & 63 : 0);
     if (key != c->cluster_key) {
-      c->cluster_val = assoc_cluster_size(n_streams, a.cap_tracks, a.cap_det, a.cap_entries);
+      c->cluster_val = a.threads == kAssocThreadsSmall ? 1 : assoc_cluster_size(n_streams, a.cap_tracks, a.cap_det, a.cap_entries);
       c->cluster_key = key;
     }
     a.cluster = c->cluster_val;
@@ -741,11 +760,12 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.cap_tracks = c->cap.max_tracks;
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
+  a.threads = c->assoc_threads;
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
-  a.stats = c->profiling ? c->d_stats : nullptr;
+  a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
   a.cluster = 1;
   a.out.count = out->count;
   a.out.track_id = reinterpret_cast<long long*>(out->track_id);
@@ -880,6 +900,13 @@ int tf_timeline(tf_ctx* c, double* out, int32_t max_updates, int32_t* n_updates)
       TF_CUDA(c, cudaEventElapsedTime(&t, c->events[4], c->events[6 * u + order[k]]));
       out[6 * u + k] = t;
     }
+  return TF_OK;
+}
+
+int tf_launch_info(tf_ctx* c, int32_t* assoc_threads, int32_t* assoc_cluster) {
+  if (!c || !assoc_threads || !assoc_cluster) return TF_ARGUMENT;
+  *assoc_threads = c->assoc_threads;
+  *assoc_cluster = c->cluster_val;
   return TF_OK;
 }
 

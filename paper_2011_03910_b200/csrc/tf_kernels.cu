@@ -936,7 +936,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       : "memory");
 }
 
-__global__ void __launch_bounds__(kAssocThreads, 1) associate_kernel(AssocArgs a, Params P) {
+// kThreads = 256: one CTA per SM (the register file is the limit), clusters
+// for few streams. kThreads = 128: two CTAs per SM for launches with more
+// streams than twice the SM count (the host halves the shared-memory plan).
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(AssocArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int C = a.cluster;                   // CTAs per stream (thread-block cluster)
   const int ls = blockIdx.x / C;             // local stream in this update
@@ -2526,7 +2530,7 @@ size_t frame_smem_bytes(int total_anchors, int cap_cand) {
 }
 size_t assoc_static_smem() {
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, associate_kernel) != cudaSuccess) return 8192;
+  if (cudaFuncGetAttributes(&fa, associate_kernel<kAssocThreads>) != cudaSuccess) return 8192;
   return fa.sharedSizeBytes;
 }
 
@@ -2646,9 +2650,14 @@ cudaError_t launch_frame_rows(const double* boxes, const double* obj, const floa
 
 cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st) {
   const size_t smem = assoc_smem_bytes(a.cap_tracks, a.cap_det, a.cap_entries);
-  set_smem(reinterpret_cast<const void*>(associate_kernel), smem);
+  if (a.threads == kAssocThreadsSmall) {
+    set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreadsSmall>), smem);
+    associate_kernel<kAssocThreadsSmall><<<n_streams, kAssocThreadsSmall, smem, st>>>(a, P);
+    return cudaGetLastError();
+  }
+  set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreads>), smem);
   if (a.cluster <= 1) {
-    associate_kernel<<<n_streams, kAssocThreads, smem, st>>>(a, P);
+    associate_kernel<kAssocThreads><<<n_streams, kAssocThreads, smem, st>>>(a, P);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -2663,7 +2672,7 @@ cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, associate_kernel, a, P);
+  return cudaLaunchKernelEx(&cfg, associate_kernel<kAssocThreads>, a, P);
 }
 
 int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entries) {
@@ -2681,8 +2690,8 @@ int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entri
   while (c > 1 && n_streams * c > sms) c >>= 1;
   if (c > 1) {
     const size_t smem = assoc_smem_bytes(cap_tracks, cap_det, cap_entries);
-    set_smem(reinterpret_cast<const void*>(associate_kernel), smem);   // (only ever raised: see set_smem)
-    if (c > 8) cudaFuncSetAttribute(associate_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreads>), smem);   // (only ever raised: see set_smem)
+    if (c > 8) cudaFuncSetAttribute(associate_kernel<kAssocThreads>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(c));
     cfg.blockDim = dim3(kAssocThreads);
@@ -2697,7 +2706,7 @@ int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entri
     // every stream's cluster must be resident at once (clusters live inside a
     // GPC; a second wave would double the update time): shrink until they fit
     int clusters = 0;
-    while (c > 1 && (cudaOccupancyMaxActiveClusters(&clusters, associate_kernel, &cfg) != cudaSuccess ||
+    while (c > 1 && (cudaOccupancyMaxActiveClusters(&clusters, associate_kernel<kAssocThreads>, &cfg) != cudaSuccess ||
                      clusters < n_streams)) {
       c >>= 1;
       cfg.gridDim = dim3(static_cast<unsigned>(c));

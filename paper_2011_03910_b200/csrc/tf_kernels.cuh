@@ -6,6 +6,7 @@
 namespace tfd {
 
 constexpr int kAssocThreads = 256;
+constexpr int kAssocThreadsSmall = 128;   // two association CTAs per SM (many streams)
 
 // Per-frame detection buffer written by the frame stage, read by associate_kernel.
 // Arrays are [frames][cap_det] (meas: x4, emb: xD).
@@ -69,6 +70,7 @@ struct AssocArgs {
   int16_t* pool_aux;             // [streams][2 * cap_tracks * cap_det] overflow edge lists
   long long* stats;              // [32] phase cycles / counters (nullptr = off)
   int cluster;                   // CTAs per stream (1 = no cluster)
+  int threads;                   // kAssocThreads, or kAssocThreadsSmall (no cluster)
 };
 
 struct HeadLaunch {

@@ -24,13 +24,22 @@ def _pkg():
     return p, synth
 
 
+def _launch_info(bt):
+    import ctypes as C
+    th, cl = C.c_int32(), C.c_int32()
+    bt.engine.lib.tf_launch_info(bt.engine.ctx, C.byref(th), C.byref(cl))
+    return th.value, cl.value
+
+
 def _run_parity(cfg_name, steps, B, streams=1, quantize=False, literal=False, config=None, max_tracks=256,
-                half=False, **synth_kw):
+                half=False, max_detections=256, expect_threads=None, **synth_kw):
     p, synth = _pkg()
     cfg = config or p.TrackerConfig()
     gen = synth.make(cfg_name, device="cuda", streams=streams, literal_noise=literal, **synth_kw)
-    cap = p.Capacity(streams=streams, max_frames=streams * B, max_tracks=max_tracks)
+    cap = p.Capacity(streams=streams, max_frames=streams * B, max_tracks=max_tracks, max_detections=max_detections)
     bt = p.BatchTracker(streams, cfg, frames_per_update=B, quantize=quantize, capacity=cap)
+    if expect_threads is not None:
+        assert _launch_info(bt)[0] == expect_threads
     oracles = [ot.OracleTracker(oracle_settings(cfg, quantize)) for _ in range(streams)]
     cmp = FrameCompare()
     frame = 0
@@ -187,6 +196,43 @@ def test_cluster_and_single_cta_association_agree(monkeypatch):
             assert np.array_equal(i1[f, :n], i8[f, :n])
             assert np.array_equal(b1[f, :n], b8[f, :n])
             assert np.array_equal(np.nan_to_num(k1[f, :n]), np.nan_to_num(k8[f, :n]))
+
+
+def test_narrow_association_ctas_match_oracle(monkeypatch):
+    """The 128-thread association CTAs (two per SM, chosen for launches with
+    more streams than twice the SM count) against the oracle, forced on a
+    small cfg3-like launch."""
+    monkeypatch.setenv("TF_ASSOC_NARROW", "1")
+    cmp = _run_parity("cfg3", steps=3, B=8, streams=6, max_tracks=192, max_detections=128, expect_threads=128)
+    assert cmp.frames == 6 * 24
+
+
+def test_narrow_and_wide_association_agree(monkeypatch):
+    """128- and 256-thread association CTAs give identical records and traces."""
+    p, synth = _pkg()
+    outs = []
+    for env in ("TF_ASSOC_NARROW", "TF_ASSOC_WIDE"):
+        monkeypatch.delenv("TF_ASSOC_NARROW", raising=False)
+        monkeypatch.delenv("TF_ASSOC_WIDE", raising=False)
+        monkeypatch.setenv(env, "1")
+        gen = synth.make("cfg4", device="cuda", streams=16, seed=5)
+        cap = p.Capacity(streams=16, max_frames=16 * 8, max_candidates=192, max_detections=96, max_tracks=160)
+        bt = p.BatchTracker(16, frames_per_update=8, capacity=cap)
+        assert _launch_info(bt)[0] == (128 if env == "TF_ASSOC_NARROW" else 256)
+        res = []
+        for _ in range(3):
+            r = bt.update(gen.next_batch(8), trace=True)
+            tr = bt.trace(16 * 8)
+            res.append((r.count.cpu().numpy().copy(), r.track_id.cpu().numpy().copy(), r.box.cpu().numpy().copy(),
+                        tr["det_cost"].cpu().numpy().copy()))
+        outs.append(res)
+    for (c1, i1, b1, k1), (c2, i2, b2, k2) in zip(*outs):
+        assert np.array_equal(c1, c2)
+        for f in range(16 * 8):
+            n = c1[f]
+            assert np.array_equal(i1[f, :n], i2[f, :n])
+            assert np.array_equal(b1[f, :n], b2[f, :n])
+            assert np.array_equal(np.nan_to_num(k1[f, :n]), np.nan_to_num(k2[f, :n]))
 
 
 def test_pipelined_updates_match_serial():
