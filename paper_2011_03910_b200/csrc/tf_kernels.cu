@@ -2060,16 +2060,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");   // no prefetch outlives an early exit
   __syncthreads();
-  // ---- release the follower CTAs (they wait at the S1 barrier) ----------------
-  if (C > 1) {
-    if (s3_pending) cluster_wait_acquire();
-    if (ema_out) mbar_wait(&s_bar[0], ph_ema_done);   // followers are done with this CTA's memory
-    if (signaller) st_cluster(F_fl, 1);               // stop
-    cluster_arrive_release();
-    cluster_wait_acquire();
-    if (tid == 0 && s_status == 0 && s_ema_err != STATUS_CLEAR) s_status = (s_ema_b << 8) | (s_ema_err & 0xff);
-  }
-  // ---- write the stream's state back -----------------------------------------
+  // ---- write the stream's state back (the followers' last EMA runs meanwhile) --
   T = s_T;
   for (int i = tid; i < s_nfree; i += blockDim.x) tb.free_stack[sT + i] = f_stk[i];
   for (int t = tid; t < T; t += blockDim.x) {
@@ -2081,6 +2072,16 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     tb.slot[sT + t] = t_slot[t];
     for (int q = 0; q < 8; ++q) tb.mean[(sT + t) * 8 + q] = t_mean[8 * t + q];
     for (int q = 0; q < 12; ++q) tb.cov[(sT + t) * 12 + q] = t_cov[12 * t + q];
+  }
+  // ---- release the follower CTAs (they wait at the S1 barrier) ----------------
+  __syncthreads();
+  if (C > 1) {
+    if (s3_pending) cluster_wait_acquire();
+    if (ema_out) mbar_wait(&s_bar[0], ph_ema_done);   // followers are done with this CTA's memory
+    if (signaller) st_cluster(F_fl, 1);               // stop
+    cluster_arrive_release();
+    cluster_wait_acquire();
+    if (tid == 0 && s_status == 0 && s_ema_err != STATUS_CLEAR) s_status = (s_ema_b << 8) | (s_ema_err & 0xff);
   }
   if (a.stats && tid < 32) atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[tid]),
                                       static_cast<unsigned long long>(s_ph[tid]));
