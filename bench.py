@@ -507,7 +507,8 @@ def run_ours(args):
                 + [(16, "lap.components_tiecheck"), (17, "lap.peeling"), (18, "lap.residual_setup"),
                    (19, "lap.warp_solves"), (20, "lap.full_restatement"), (21, "cost.s1_wait"),
                    (22, "cost.leader_work"), (23, "cost.s2_wait"), (24, "cost.ema_wait"), (25, "cost.go_signal"),
-                   (26, "ema_signal"), (30, "births_tail"), (31, "whole_frame")]},
+                   (26, "ema_signal"), (30, "births_tail"), (31, "whole_frame"),
+                   (28, "launch.prologue"), (29, "launch.epilogue")]},
             "assoc_counters_per_frame": {name: float(phase[i]) / max(phase[11], 1) for i, name in
                                          [(8, "tie_fallback"), (9, "finite_entries"), (10, "multi_components"),
                                           (14, "residual_entries"), (12, "tracks"), (13, "detections"), (15, "peel_rounds")]},

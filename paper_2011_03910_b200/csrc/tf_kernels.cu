@@ -942,6 +942,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 template <int kThreads>
 __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(AssocArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const long long t_k0 = clock64();           // launch prologue / epilogue timers (slots 28, 29)
   const int C = a.cluster;                   // CTAs per stream (thread-block cluster)
   const int ls = blockIdx.x / C;             // local stream in this update
   const int s = a.stream_begin + ls;         // global stream id
@@ -1186,6 +1187,8 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   if (a.B > 0) prefetch_dets(0, d_meas0, d_obj0);
 
   long long t_top = 0;
+  if (a.stats && tid == 0) s_ph[28] += clock64() - t_k0;
+  long long t_epi = 0;
   for (int b = 0; b < a.B; ++b) {
     if (a.stats && tid == 0) {                     // whole-frame cycles (slot 31)
       const long long now_ = clock64();
@@ -2058,6 +2061,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       break;
     }
   }
+  if (a.stats && tid == 0) t_epi = clock64();
   asm volatile("cp.async.wait_all;\n" ::: "memory");   // no prefetch outlives an early exit
   __syncthreads();
   // ---- write the stream's state back (the followers' last EMA runs meanwhile) --
@@ -2083,6 +2087,8 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     cluster_wait_acquire();
     if (tid == 0 && s_status == 0 && s_ema_err != STATUS_CLEAR) s_status = (s_ema_b << 8) | (s_ema_err & 0xff);
   }
+  if (a.stats && tid == 0) s_ph[29] += clock64() - t_epi;
+  __syncthreads();
   if (a.stats && tid < 32) atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[tid]),
                                       static_cast<unsigned long long>(s_ph[tid]));
   if (tid == 0) {
