@@ -64,7 +64,14 @@ typedef struct tf_config {
   int32_t min_hits;               /* 1 */
   int32_t embedding_dim;          /* 512; any D >= 1 */
   int32_t quantize_binary16;      /* 1 = MIXED: fp16-quantise + renormalise detection embeddings */
-  int32_t reserved;
+  /* JDE extensions the reference does not have (SURVEY.md section 8 name
+   * map; off = the reference path, parity with the reference). Zero-filled
+   * fields keep them off. */
+  int32_t iou_stage;              /* 1: second association stage on 1 - IoU for tracks ACTIVE before the
+                                     frame and detections left unmatched, pairs above iou_threshold dissolved */
+  double motion_lambda;           /* lambda-fused cost lambda * cosine + motion_weight * gate distance ... */
+  double motion_weight;           /* ... with motion_weight = 1 - lambda (as the caller computes it); 0 = off */
+  double iou_threshold;           /* second-stage threshold on 1 - IoU (JDE: 0.5) */
 } tf_config;
 
 /* Fixed device capacities. Exceeding one returns TF_CAPACITY. */

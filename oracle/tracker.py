@@ -57,6 +57,12 @@ class Settings:
     std_aspect_velocity: float = 1e-5
     std_aspect_measurement: float = 1e-1
     quantize: bool = False
+    # JDE extensions, NOT in the reference (SURVEY.md section 8 name map):
+    # defaults are the reference path. Their semantics are defined by this
+    # restatement (parity unpinned: no reference implementation exists).
+    motion_lambda: float = 1.0          # cost = lambda * cosine + (1 - lambda) * gate distance
+    iou_stage: bool = False             # second stage on 1 - IoU
+    iou_threshold: float = 0.5
 
 
 # ---------------------------------------------------------------------------
@@ -337,6 +343,7 @@ class OracleTracker:
         self.removed_ids: set[int] = set()
         self.next_id = 1
         self.last_frame: int | None = None
+        self.stage2_matches = 0                 # IoU-stage matches (extension), for tests
 
     def _gates(self, meas: np.ndarray) -> np.ndarray:
         """tf/tracker.py:161-170."""
@@ -347,6 +354,26 @@ class OracleTracker:
             delta = centers[:, None, :] - meas[None, :, :2]
             return np.sum(delta * delta, axis=2)
         raise OracleError("ConfigError", f"gate metric {self.s.gate_metric!r}")
+
+    def _iou_stage(self, matches, ur, uc, meas):
+        """JDE's IoU association (extension): tracks ACTIVE before this frame
+        and unmatched by the first stage x detections still unmatched, both
+        ascending; cost 1 - IoU of the predicted track box and the detection's
+        box recovered from its measurement; the first stage's exact solve, then
+        pairs above ``iou_threshold`` dissolved."""
+        rows = [r for r in ur if self.tracks[r].state == ACTIVE]
+        if not rows or not uc:
+            return matches, ur, uc
+        tb = [from_measurement(self.tracks[r].mean[:4]) for r in rows]
+        db = [from_measurement(meas[c]) for c in uc]
+        iou_cost = np.array([[1.0 - box_iou(a, b) for b in db] for a in tb], dtype=np.float64)
+        m2, _, _ = solve_assignment(iou_cost)
+        m2, _, _ = threshold_matches(m2, [], [], self.s.iou_threshold)
+        self.stage2_matches += len(m2)
+        got_r = {rows[i] for i, _, _ in m2}
+        got_c = {uc[j] for _, j, _ in m2}
+        matches = list(matches) + [(rows[i], uc[j], v) for i, j, v in m2]
+        return (matches, [r for r in ur if r not in got_r], [c for c in uc if c not in got_c])
 
     def step(self, frame_index: int, dets: list[Det]) -> StepTrace:
         """tf/tracker.py:85-159."""
@@ -372,9 +399,13 @@ class OracleTracker:
         cost = cosine_costs([t.emb for t in self.tracks], [d.embedding for d in live])
         if self.tracks and live:
             g = self._gates(meas)
+            if s.motion_lambda != 1.0:                            # JDE fuse_motion (extension)
+                cost = s.motion_lambda * cost + (1.0 - s.motion_lambda) * g
             cost = np.where(g > s.gate_threshold, np.inf, cost)   # tf/assoc.py:49-57
         m, ur, uc = solve_assignment(cost)
         matches, ur, uc = threshold_matches(m, ur, uc, s.max_cost)
+        if s.iou_stage:
+            matches, ur, uc = self._iou_stage(matches, ur, uc, meas)
 
         emitted = []
         match_ids = []

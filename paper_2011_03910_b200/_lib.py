@@ -23,7 +23,8 @@ class TfConfig(C.Structure):
         ("smoothing_alpha", c_dbl), ("std_weight_position", c_dbl), ("std_weight_velocity", c_dbl),
         ("std_aspect", c_dbl), ("std_aspect_velocity", c_dbl), ("std_aspect_measurement", c_dbl),
         ("gate_metric", c_i32), ("max_lost", c_i32), ("min_hits", c_i32), ("embedding_dim", c_i32),
-        ("quantize_binary16", c_i32), ("reserved", c_i32),
+        ("quantize_binary16", c_i32), ("iou_stage", c_i32),
+        ("motion_lambda", c_dbl), ("motion_weight", c_dbl), ("iou_threshold", c_dbl),
     ]
 
 

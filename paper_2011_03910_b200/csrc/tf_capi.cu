@@ -146,6 +146,11 @@ Params make_params(const tf_config& c) {
   p.min_hits = c.min_hits;
   p.dim = c.embedding_dim;
   p.quantize = c.quantize_binary16;
+  p.fuse = c.motion_weight != 0.0;
+  p.lambda = c.motion_lambda;
+  p.lambda_w = c.motion_weight;
+  p.iou_stage = c.iou_stage != 0;
+  p.iou_threshold = c.iou_threshold;
   return p;
 }
 
@@ -157,6 +162,10 @@ int check_step_config(tf_ctx* c) {
     return fail(c, TF_CONFIG, "confidence threshold must be in [0, 1], got " + std::to_string(g.conf_threshold));
   if (!(g.nms_iou > 0.0 && g.nms_iou < 1.0))
     return fail(c, TF_CONFIG, "NMS IoU threshold must be in (0, 1), got " + std::to_string(g.nms_iou));
+  if (g.motion_weight != 0.0 && !(g.motion_lambda >= 0.0 && g.motion_lambda <= 1.0))
+    return fail(c, TF_CONFIG, "motion lambda must be in [0, 1], got " + std::to_string(g.motion_lambda));
+  if (g.iou_stage && !(g.iou_threshold >= 0.0 && g.iou_threshold <= 1.0))
+    return fail(c, TF_CONFIG, "second-stage IoU threshold must be in [0, 1], got " + std::to_string(g.iou_threshold));
   return TF_OK;
 }
 

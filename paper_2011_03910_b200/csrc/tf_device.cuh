@@ -30,6 +30,11 @@ struct Params {
   double std_aspect, std_aspect_velocity, std_aspect_measurement;
   int gate_metric;         // 0 mahalanobis, 1 euclidean, other -> ConfigError when used
   int max_lost, min_hits, dim, quantize;
+  // JDE extensions (off = the reference): lambda-fused cost and a second
+  // association stage on 1 - IoU
+  double lambda, lambda_w;  // cost = lambda * cosine + lambda_w * gate distance when fuse
+  double iou_threshold;
+  int fuse, iou_stage;
 };
 
 // ---------------------------------------------------------------- misc

@@ -656,6 +656,130 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
 }
 
 
+// ---- JDE extensions (off on the reference path; SURVEY.md section 8 name map)
+
+// lambda-fused cost (JDE fuse_motion): every un-gated entry becomes
+// lambda * cosine + (1 - lambda) * gate distance, the distance recomputed with
+// the gate phase's arithmetic. Called by every thread of the leader; leaves
+// the per-warp maxima of the fused costs in ampw[0 .. n_slots).
+__device__ __noinline__ void fuse_motion_costs(double lambda, double lambda_w, int gate_metric, const int16_t* ecol,
+                                               const int16_t* erow, double* eval, int E, const double* t_mean,
+                                               const double* g_il, const double* d_meas, double* ampw, int n_slots) {
+  double m = 0.0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int t = erow[e], k = ecol[e];
+    const double* mu = &t_mean[8 * t];
+    const double* z = &d_meas[4 * k];
+    double g;
+    if (gate_metric == 0) {
+      g = KF::mahalanobis(mu, &g_il[4 * t], z);
+    } else {
+      const double dx = mu[0] - z[0], dy = mu[1] - z[1];
+      g = dx * dx + dy * dy;
+    }
+    const double v = lambda * eval[e] + lambda_w * g;
+    eval[e] = v;
+    m = fmax(m, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+  if (lane_id() == 0) ampw[warp_id()] = m;
+  for (int i = n_warps() + threadIdx.x; i < n_slots; i += blockDim.x) ampw[i] = 0.0;
+}
+
+// Dense rows of the second-stage matrix for the exact LAP.
+struct DenseRows {
+  const double* m;
+  int nc;
+  __device__ __forceinline__ int begin(int r) const { return r * nc; }
+  __device__ __forceinline__ int end(int r) const { return r * nc + nc; }
+  __device__ __forceinline__ int col(int e) const { return e % nc; }
+  __device__ __forceinline__ double val(int e) const { return m[e]; }
+};
+
+// Second association stage on 1 - IoU (JDE's IoU step): tracks that were
+// ACTIVE before the frame and are unmatched after the first stage, against the
+// detections still unmatched, both in ascending order; boxes from the
+// predicted track state and from the detections' measurements. The same exact
+// solve as the first stage (sentinel padding, scipy order), then pairs above
+// iou_threshold are dissolved. One warp.
+__device__ __noinline__ void iou_second_stage(double thr, int T, int K, int Tm, int Km, int cap_entries,
+                                              unsigned char* smem, const double* d_meas, double* dense_global,
+                                              int* err) {
+  const int lane = lane_id();
+  const AssocPlan pl = assoc_plan(Tm, Km, cap_entries);
+  const double* t_mean = reinterpret_cast<const double*>(smem + pl.off_mean);
+  const int* t_state = reinterpret_cast<const int*>(smem + pl.off_state);
+  int* t_mdet = reinterpret_cast<int*>(smem + pl.off_mdet);
+  double* t_mcost = reinterpret_cast<double*>(smem + pl.off_mcost);
+  int* d_row = reinterpret_cast<int*>(smem + pl.off_drow);
+  int16_t* rows = reinterpret_cast<int16_t*>(smem + pl.off_crows);
+  int16_t* cols = reinterpret_cast<int16_t*>(smem + pl.off_ccols);
+  double* dense_smem = reinterpret_cast<double*>(smem + pl.off_eval);
+  const int dense_cap = cap_entries;
+  LapScratch L;
+  L.u = reinterpret_cast<double*>(smem + pl.off_u);
+  L.v = reinterpret_cast<double*>(smem + pl.off_v);
+  L.dist = reinterpret_cast<double*>(smem + pl.off_dist);
+  L.crow = reinterpret_cast<double*>(smem + pl.off_crow);
+  L.path = reinterpret_cast<int16_t*>(smem + pl.off_path);
+  L.row4col = reinterpret_cast<int16_t*>(smem + pl.off_r4c);
+  L.col4row = reinterpret_cast<int16_t*>(smem + pl.off_c4r);
+  L.rem = reinterpret_cast<int16_t*>(smem + pl.off_rem);
+  L.vrows = reinterpret_cast<int16_t*>(smem + pl.off_vr);
+  L.vcols = reinterpret_cast<int16_t*>(smem + pl.off_vc);
+  int nr = 0, nc = 0;
+  for (int t0 = 0; t0 < T; t0 += 32) {                 // ordered compaction of the lists
+    const int t = t0 + lane;
+    const bool in = t < T && t_mdet[t] < 0 && t_state[t] == 0;
+    const unsigned bm = __ballot_sync(FULL, in);
+    if (in) rows[nr + __popc(bm & ((1u << lane) - 1u))] = static_cast<int16_t>(t);
+    nr += __popc(bm);
+  }
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    const int k = k0 + lane;
+    const bool in = k < K && d_row[k] < 0;
+    const unsigned bm = __ballot_sync(FULL, in);
+    if (in) cols[nc + __popc(bm & ((1u << lane) - 1u))] = static_cast<int16_t>(k);
+    nc += __popc(bm);
+  }
+  __syncwarp();
+  if (nr == 0 || nc == 0) return;
+  double* dense = nr * nc <= dense_cap ? dense_smem : dense_global;
+  double amp = 0.0;
+  for (int x = lane; x < nr * nc; x += 32) {
+    const int i = x / nc, j = x - i * nc;
+    double a[4], b[4];
+    const bool oka = meas_to_box(&t_mean[8 * rows[i]], a);
+    const bool okb = meas_to_box(&d_meas[4 * cols[j]], b);
+    if (!oka) flag_error(err, rows[i] + 1, TF_INVALID_BOX);
+    if (!okb) flag_error(err, cols[j] + 1, TF_INVALID_BOX);
+    const double v = 1.0 - iou_tlwh(a[0], a[1], a[2], a[3], b[0], b[1], b[2], b[3]);
+    dense[x] = v;
+    amp = fmax(amp, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amp = fmax(amp, __shfl_xor_sync(FULL, amp, o));
+  __syncwarp();
+  const int n = nr > nc ? nr : nc;
+  const double sentinel = 2.0 * static_cast<double>(n) * fmax(amp, 1.0) + 1.0;   // tf/assoc.py:67-74
+  warp_lap_fast(n, nr, DenseRows{dense, nc}, sentinel, L);
+  __syncwarp();
+  for (int i = lane; i < nr; i += 32) {
+    const int c = L.col4row[i];
+    if (c < nc) {
+      const double v = dense[i * nc + c];
+      if (!(v > thr)) {                                   // tf/assoc.py:90-107 with the stage's threshold
+        const int t = rows[i], k = cols[c];
+        t_mdet[t] = k;
+        t_mcost[t] = v;
+        d_row[k] = t;
+      }
+    }
+  }
+  __syncwarp();
+}
+
 // Embedding rows of a frame's births, one warp per birth: each new track's
 // pool slot (popped in birth order) receives its detection's embedding. Out
 // of line so the row held in registers does not weigh on the kernel's
@@ -939,7 +1063,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // kThreads = 256: one CTA per SM (the register file is the limit), clusters
 // for few streams. kThreads = 128: two CTAs per SM for launches with more
 // streams than twice the SM count (the host halves the shared-memory plan).
-template <int kThreads>
+// kExt: the JDE extensions (lambda-fused cost, IoU second stage) are compiled
+// only into their own instantiations, so the reference path keeps its code.
+template <int kThreads, bool kExt>
 __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(AssocArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const long long t_k0 = clock64();           // launch prologue / epilogue timers (slots 28, 29)
@@ -1392,6 +1518,11 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       }
     }
     TF_SUB(23);
+    if (kExt && P.fuse && s_Efr > 0) {    // JDE extension: lambda-fused cost (off on the reference path)
+      fuse_motion_costs(P.lambda, P.lambda_w, P.gate_metric, ecol, erow, eval, s_Efr, t_mean, g_il, d_meas, s_ampw,
+                        nw * C);
+      __syncthreads();
+    }
     // the previous frame's EMA list was consumed before S1: reset it
     for (int k = tid; k < K; k += blockDim.x) ema_slot[k] = -1;
     if (wid == 0) {                       // amplitude of the finite costs (read by the LAP after barriers)
@@ -1842,10 +1973,37 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     // matched tracks' Kalman update + lifecycle (tf/tracker.py:114-143), one
     // thread per track in one pass; matched tracks also post their EMA work
     TF_MARK(5);
+    if (kExt && P.iou_stage) {
+      // JDE extension: first-stage matches, then the IoU stage on what is left
+      for (int t = tid; t < T; t += blockDim.x) {
+        int md = -1;
+        double mc = 0.0;
+        const int c = gating ? rcol[t] : -1;
+        if (c >= 0) {
+          for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
+            if (ecol[e] == c) {
+              mc = eval[e];
+              md = (mc > P.max_cost) ? -1 : c;
+              break;
+            }
+        }
+        t_mdet[t] = md;
+        t_mcost[t] = mc;
+        if (md >= 0) d_row[md] = t;
+      }
+      __syncthreads();
+      if (wid == 0 && T > 0 && K > 0)
+        iou_second_stage(P.iou_threshold, T, K, Tm, Km, a.cap_entries, smem, d_meas,
+                         a.pool_val + static_cast<long long>(s) * Tm * Km, &s_err);
+      __syncthreads();
+    }
     for (int t = tid; t < T; t += blockDim.x) {
       int md = -1;
       double mc = 0.0;
-      if (gating) {
+      if (kExt && P.iou_stage) {
+        md = t_mdet[t];
+        mc = t_mcost[t];
+      } else if (gating) {
         const int c = rcol[t];
         if (c >= 0) {
           for (int e = rowptr[t]; e < rowptr[t + 1]; ++e)
@@ -2537,7 +2695,7 @@ size_t frame_smem_bytes(int total_anchors, int cap_cand) {
 }
 size_t assoc_static_smem() {
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, associate_kernel<kAssocThreads>) != cudaSuccess) return 8192;
+  if (cudaFuncGetAttributes(&fa, associate_kernel<kAssocThreads, false>) != cudaSuccess) return 8192;
   return fa.sharedSizeBytes;
 }
 
@@ -2655,17 +2813,24 @@ cudaError_t launch_frame_rows(const double* boxes, const double* obj, const floa
   return cudaGetLastError();
 }
 
-cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st) {
+template <bool kExt>
+static cudaError_t launch_associate_t(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st) {
   const size_t smem = assoc_smem_bytes(a.cap_tracks, a.cap_det, a.cap_entries);
   if (a.threads == kAssocThreadsSmall) {
-    set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreadsSmall>), smem);
-    associate_kernel<kAssocThreadsSmall><<<n_streams, kAssocThreadsSmall, smem, st>>>(a, P);
+    set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreadsSmall, kExt>), smem);
+    associate_kernel<kAssocThreadsSmall, kExt><<<n_streams, kAssocThreadsSmall, smem, st>>>(a, P);
     return cudaGetLastError();
   }
-  set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreads>), smem);
+  set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreads, kExt>), smem);
   if (a.cluster <= 1) {
-    associate_kernel<kAssocThreads><<<n_streams, kAssocThreads, smem, st>>>(a, P);
+    associate_kernel<kAssocThreads, kExt><<<n_streams, kAssocThreads, smem, st>>>(a, P);
     return cudaGetLastError();
+  }
+  if (kExt && a.cluster > 8) {          // (the reference-path instantiation is set up by assoc_cluster_size)
+    static bool nonportable = false;
+    if (!nonportable)
+      cudaFuncSetAttribute(associate_kernel<kAssocThreads, kExt>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    nonportable = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(n_streams * a.cluster));
@@ -2679,7 +2844,12 @@ cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, associate_kernel<kAssocThreads>, a, P);
+  return cudaLaunchKernelEx(&cfg, associate_kernel<kAssocThreads, kExt>, a, P);
+}
+
+cudaError_t launch_associate(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st) {
+  return (P.fuse || P.iou_stage) ? launch_associate_t<true>(a, n_streams, P, st)
+                                 : launch_associate_t<false>(a, n_streams, P, st);
 }
 
 int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entries) {
@@ -2697,8 +2867,8 @@ int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entri
   while (c > 1 && n_streams * c > sms) c >>= 1;
   if (c > 1) {
     const size_t smem = assoc_smem_bytes(cap_tracks, cap_det, cap_entries);
-    set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreads>), smem);   // (only ever raised: see set_smem)
-    if (c > 8) cudaFuncSetAttribute(associate_kernel<kAssocThreads>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreads, false>), smem);   // (only ever raised: see set_smem)
+    if (c > 8) cudaFuncSetAttribute(associate_kernel<kAssocThreads, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(c));
     cfg.blockDim = dim3(kAssocThreads);
@@ -2713,7 +2883,7 @@ int assoc_cluster_size(int n_streams, int cap_tracks, int cap_det, int cap_entri
     // every stream's cluster must be resident at once (clusters live inside a
     // GPC; a second wave would double the update time): shrink until they fit
     int clusters = 0;
-    while (c > 1 && (cudaOccupancyMaxActiveClusters(&clusters, associate_kernel<kAssocThreads>, &cfg) != cudaSuccess ||
+    while (c > 1 && (cudaOccupancyMaxActiveClusters(&clusters, associate_kernel<kAssocThreads, false>, &cfg) != cudaSuccess ||
                      clusters < n_streams)) {
       c >>= 1;
       cfg.gridDim = dim3(static_cast<unsigned>(c));

@@ -39,7 +39,12 @@ def make_config(cfg, quantize: bool = False) -> _lib.TfConfig:
         # as the reference rejects them lazily in _gate_matrix (tf/tracker.py:161-170)
         gate_metric=GATE_METRICS.get(cfg.gate_metric, 2), max_lost=int(cfg.max_lost),
         min_hits=int(cfg.min_hits), embedding_dim=int(cfg.embedding_dim),
-        quantize_binary16=int(bool(quantize)), reserved=0)
+        quantize_binary16=int(bool(quantize)),
+        # JDE extensions (off by default: the reference path)
+        iou_stage=int(bool(getattr(cfg, "iou_stage", False))),
+        motion_lambda=float(getattr(cfg, "motion_lambda", 1.0)),
+        motion_weight=1.0 - float(getattr(cfg, "motion_lambda", 1.0)),
+        iou_threshold=float(getattr(cfg, "iou_threshold", 0.5)))
 
 
 class Engine:

@@ -61,6 +61,13 @@ class TrackerConfig:
     min_hits: int = 1
     embedding_dim: int = EMBEDDING_DIM
     motion_noise: MotionNoise = MotionNoise()
+    # JDE extensions the reference does not have (off = the reference path):
+    # lambda-fused cost lambda * cosine + (1 - lambda) * gate distance, and a
+    # second association stage on 1 - IoU (tracks ACTIVE before the frame x
+    # detections left unmatched, pairs above iou_threshold dissolved)
+    motion_lambda: float = 1.0
+    iou_stage: bool = False
+    iou_threshold: float = 0.5
 
 
 @dataclass(frozen=True)

@@ -23,7 +23,9 @@ def oracle_settings(cfg, quantize=False) -> ot.Settings:
                        embedding_dim=cfg.embedding_dim, std_weight_position=n.std_weight_position,
                        std_weight_velocity=n.std_weight_velocity, std_aspect=n.std_aspect,
                        std_aspect_velocity=n.std_aspect_velocity,
-                       std_aspect_measurement=n.std_aspect_measurement, quantize=quantize)
+                       std_aspect_measurement=n.std_aspect_measurement, quantize=quantize,
+                       motion_lambda=getattr(cfg, "motion_lambda", 1.0), iou_stage=getattr(cfg, "iou_stage", False),
+                       iou_threshold=getattr(cfg, "iou_threshold", 0.5))
 
 
 class FrameCompare:

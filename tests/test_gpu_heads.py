@@ -235,6 +235,43 @@ def test_narrow_and_wide_association_agree(monkeypatch):
             assert np.array_equal(np.nan_to_num(k1[f, :n]), np.nan_to_num(k2[f, :n]))
 
 
+def _run_ext(cfg_name, config, **kw):
+    """_run_parity, also returning the oracle's IoU-stage match count."""
+    import oracle.tracker as ot
+    counts = []
+    orig = ot.OracleTracker.__init__
+
+    def init(self, settings=None):
+        orig(self, settings)
+        counts.append(self)
+    ot.OracleTracker.__init__ = init
+    try:
+        cmp = _run_parity(cfg_name, config=config, **kw)
+    finally:
+        ot.OracleTracker.__init__ = orig
+    return cmp, sum(o.stage2_matches for o in counts)
+
+
+def test_jde_extensions_match_oracle():
+    """lambda-fused cost + IoU second stage (JDE extensions, off on the
+    reference path) against the oracle's restatement of them."""
+    p, _ = _pkg()
+    cfg = p.TrackerConfig(motion_lambda=0.98, iou_stage=True, iou_threshold=0.5)
+    cmp, _ = _run_ext("cfg1", cfg, steps=4, B=8)
+    assert cmp.frames == 32 and cmp.matches > 0
+
+
+def test_iou_stage_takes_over_dissolved_matches():
+    """A strict cosine threshold dissolves most first-stage matches; the IoU
+    stage re-associates them, exactly as the oracle does."""
+    p, _ = _pkg()
+    cfg = p.TrackerConfig(max_cost=0.02, motion_lambda=0.98, iou_stage=True, iou_threshold=0.5)
+    cmp, n2 = _run_ext("cfg1", cfg, steps=3, B=8)
+    assert n2 > 50, n2
+    cmp, n2 = _run_ext("cfg3", cfg, steps=2, B=8, streams=6)
+    assert n2 > 20, n2
+
+
 def test_pipelined_updates_match_serial():
     """Pipelining (decode of update i+1 overlapping association of update i on
     a side stream, double-buffered detections) gives the serial results."""
