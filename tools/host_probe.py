@@ -35,6 +35,26 @@ ev1.record()
 torch.cuda.synchronize()
 print(f"B={B}: host {1e6 * (t1 - t0) / (N // 2):.1f} us per update call, "
       f"GPU {1e3 * ev0.elapsed_time(ev1) / (N // 2):.1f} us per update")
+# time spent inside the C entry point alone
+lib0 = bt.engine.lib
+orig = lib0.tf_update_heads
+acc = [0.0, 0]
+
+
+def timed(*args):
+    t = time.perf_counter()
+    r = orig(*args)
+    acc[0] += time.perf_counter() - t
+    acc[1] += 1
+    return r
+
+
+lib0.tf_update_heads = timed
+for i in range(10, 10 + N // 2):
+    bt.update(batches[i], sync=False)
+bt.join()
+lib0.tf_update_heads = orig
+print(f"inside tf_update_heads: {1e6 * acc[0] / max(acc[1], 1):.1f} us per call")
 pr = cProfile.Profile()
 pr.enable()
 for i in range(10 + N // 2, 10 + N):
