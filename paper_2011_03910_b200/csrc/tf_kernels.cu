@@ -2387,18 +2387,30 @@ __global__ void __launch_bounds__(kKfBlock) kalman_kernel(int op, int n, Params 
   double* TB = kf_smem + kKfBlock * kKfPad;           // [64][65] scratch, then outputs
   const int tid = threadIdx.x, i0 = blockIdx.x * kKfBlock, i = i0 + tid;
   const int nb = min(kKfBlock, n - i0);
-  if (op != 0)
-    for (int x = tid; x < nb * 64; x += kKfBlock) TA[(x >> 6) * kKfPad + (x & 63)] = cov_in[64LL * i0 + x];
+  // the block's 64 covariances are one contiguous 32 KB range: every 8-byte
+  // piece is in flight at once (cp.async), the per-state mean and measurement
+  // loads overlap them
+  if (op != 0) {
+    const double* src = cov_in + 64LL * i0;
+    for (int x = tid; x < nb * 64; x += kKfBlock)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(TA + (x >> 6) * kKfPad + (x & 63))),
+                   "l"(src + x)
+                   : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  double m[8], z[4];
+  if (i < n) {
+    if (op != 0)
+      for (int q = 0; q < 8; ++q) m[q] = mean_in[8LL * i + q];
+    if (op == 0 || op == 3)
+      for (int q = 0; q < 4; ++q) z[q] = zin[4LL * i + q];
+  }
+  if (op != 0) asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   const int out_w = op == 2 ? 16 : 64;                // output covariance elements per state
   double* c = TA + tid * kKfPad;
   double* o = TB + tid * kKfPad;
   if (i < n) {
-    double m[8], z[4];
-    if (op != 0)
-      for (int q = 0; q < 8; ++q) m[q] = mean_in[8LL * i + q];
-    if (op == 0 || op == 3)
-      for (int q = 0; q < 4; ++q) z[q] = zin[4LL * i + q];
     int st = 0;
     if (op == 0) {
       double h = z[3];
