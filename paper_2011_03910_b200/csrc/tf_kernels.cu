@@ -2615,6 +2615,41 @@ __global__ void normalize_rows_kernel(int n, int dim, const double* in64, const 
   const int r = blockIdx.x * n_warps() + warp_id();
   if (r >= n) return;
   const int lane = lane_id();
+  if (in32 && dim == 512 && !quantize) {
+    // fp32 rows of 512: the row is read once into registers (same per-lane
+    // element order and summation as below, so bit-identical results) and
+    // divided with one reciprocal per row (div_by: the correctly rounded
+    // quotient, exact true division when the norm is far from the exponent
+    // limits; plain division otherwise)
+    const float* src = in32 + r * stride;
+    float xs[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) xs[k] = src[lane + 32 * k];
+    double ss = 0.0;
+    bool fin = true;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double v = static_cast<double>(xs[k]);
+      fin = fin && isfinite(v);
+      ss += v * v;
+    }
+    ss = warp_sum(ss);
+    fin = __all_sync(FULL, fin);
+    const double nrm = sqrt(ss);
+    const int st = (!fin || nrm < 1e-12) ? TF_DEGENERATE_EMBEDDING : 0;
+    if (!st) {
+      float* o = out + static_cast<long long>(r) * dim;
+      const bool safe = nrm > 0x1p-500 && nrm < 0x1p500;
+      const double rn = __drcp_rn(nrm);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const double v = static_cast<double>(xs[k]);
+        o[lane + 32 * k] = static_cast<float>(safe ? div_by(v, nrm, rn) : v / nrm);
+      }
+    }
+    if (lane == 0) status[r] = st;
+    return;
+  }
   double ss = 0.0;
   bool fin = true;
   for (int i = lane; i < dim; i += 32) {
