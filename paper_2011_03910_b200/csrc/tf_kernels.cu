@@ -2538,6 +2538,107 @@ __global__ void __launch_bounds__(kKfBlock) kalman_kernel(int op, int n, Params 
   }
 }
 
+// Predict (op 1) of the batch API, one state per thread held in registers:
+// 16-byte loads of the thread's 512-byte covariance (L1 merges a warp's rows),
+// the same expressions as kalman_kernel's predict (finite inputs: the two
+// nonzero terms of F P and (F P) F^T; otherwise the dense sums), symmetrised
+// in place ((a + b) / 2 is symmetric in a and b).
+__global__ void __launch_bounds__(128) kalman_predict_kernel(int n, Params P, const double* mean_in,
+                                                             const double* cov_in, double* mean_out,
+                                                             double* cov_out, int* status) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double c[64];
+  const double2* src = reinterpret_cast<const double2*>(cov_in + 64LL * i);
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const double2 v = src[q];
+    c[2 * q] = v.x;
+    c[2 * q + 1] = v.y;
+  }
+  double m[8];
+  const double2* msrc = reinterpret_cast<const double2*>(mean_in + 8LL * i);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 v = msrc[q];
+    m[2 * q] = v.x;
+    m[2 * q + 1] = v.y;
+  }
+  const double h = m[3];
+  double mo[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = acc + kf_F(r, k) * m[k];
+    mo[r] = acc;
+  }
+  bool finite = true;
+#pragma unroll
+  for (int q = 0; q < 64; ++q) finite = finite && isfinite(c[q]);
+  if (finite) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c[8 * r + j] = c[8 * r + j] + c[8 * (r + 4) + j];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[8 * r + j] = c[8 * r + j] + c[8 * r + j + 4];
+  } else {
+    // dense sums (0 * inf = NaN propagates as in the reference), one column
+    // of F P at a time so everything stays in registers
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double col[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = acc + kf_F(r, k) * c[8 * k + j];
+        col[r] = acc;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) c[8 * r + j] = col[r];
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      double row[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = acc + c[8 * r + k] * kf_F(j, k);
+        row[j] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) c[8 * r + j] = row[j];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double sp = KF::qpos(P, q, h), sv = KF::qvel(P, q, h);
+    c[9 * q] = c[9 * q] + sp * sp;
+    c[9 * (q + 4)] = c[9 * (q + 4)] + sv * sv;
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k >= r) {
+        const double a = (c[8 * r + k] + c[8 * k + r]) / 2.0;
+        c[8 * r + k] = a;
+        c[8 * k + r] = a;
+      }
+  double2* dst = reinterpret_cast<double2*>(cov_out + 64LL * i);
+#pragma unroll
+  for (int q = 0; q < 32; ++q) dst[q] = make_double2(c[2 * q], c[2 * q + 1]);
+  double2* mdst = reinterpret_cast<double2*>(mean_out + 8LL * i);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) mdst[q] = make_double2(mo[2 * q], mo[2 * q + 1]);
+  status[i] = 0;
+}
+
 __global__ void gating_kernel(int nt, const double* means, const double* covs, int nm, const double* z,
                               int metric, Params P, double* out, int* status) {
   const int t = blockIdx.x;
@@ -2964,6 +3065,12 @@ cudaError_t launch_lap_dense(int n, const int* shapes, const long long* cost_off
 cudaError_t launch_kalman(int op, int n, const Params& P, const double* mi, const double* ci, const double* z,
                           double* mo, double* co, int* status, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
+  if (op == 1 && !getenv("TF_KF_TILED") && (reinterpret_cast<uintptr_t>(mi) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(ci) & 15) == 0 && (reinterpret_cast<uintptr_t>(mo) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(co) & 15) == 0) {
+    kalman_predict_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, P, mi, ci, mo, co, status);
+    return cudaGetLastError();
+  }
   const size_t smem = 2 * sizeof(double) * kKfBlock * kKfPad;
   cudaFuncSetAttribute(kalman_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   kalman_kernel<<<(n + kKfBlock - 1) / kKfBlock, kKfBlock, smem, st>>>(op, n, P, mi, ci, z, mo, co, status);
