@@ -2477,64 +2477,92 @@ __global__ void __launch_bounds__(kKfBlock) kalman_kernel(int op, int n, Params 
       } else {
         // Cholesky (lower), diagonal reciprocal as LAPACK/OpenBLAS applies it
         double inv[4];
-        for (int j = 0; j < 4 && !st; ++j) {
+        bool chol_ok = true;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
           double acc = S[5 * j];
+#pragma unroll
           for (int k = 0; k < j; ++k) acc = acc - Lc[4 * j + k] * Lc[4 * j + k];
-          if (!(acc > 0.0)) { st = TF_NUMERIC; break; }
+          chol_ok = chol_ok && (acc > 0.0);
           Lc[5 * j] = sqrt(acc);
           inv[j] = 1.0 / Lc[5 * j];
+#pragma unroll
           for (int r = j + 1; r < 4; ++r) {
             double v = S[4 * r + j];
+#pragma unroll
             for (int k = 0; k < j; ++k) v = v - Lc[4 * r + k] * Lc[4 * j + k];
             Lc[4 * r + j] = v * inv[j];
           }
         }
+        if (!chol_ok) st = TF_NUMERIC;
         if (!st) {
-          // gain^T = S^-1 (P H^T)^T via L then L^T solves, column by column (G in o[0..31])
-          double* G = o;   // [4][8]
+          // gain^T = S^-1 (P H^T)^T via L then L^T solves, column by column
+          // (G [4][8] in registers; the result is written over P in place, so
+          // the block needs one shared tile)
+          double G[32];
+#pragma unroll
           for (int col = 0; col < 8; ++col) {
             double y[4];
+#pragma unroll
             for (int r = 0; r < 4; ++r) {
               double v = c[8 * col + r];        // (P H^T)^T [r][col] = P[col][r]
+#pragma unroll
               for (int k = 0; k < r; ++k) v = v - Lc[4 * r + k] * y[k];
               y[r] = v * inv[r];
             }
+#pragma unroll
             for (int r = 3; r >= 0; --r) {
               double v = y[r];
+#pragma unroll
               for (int k = r + 1; k < 4; ++k) v = v - Lc[4 * k + r] * G[8 * k + col];
               G[8 * r + col] = v * inv[r];
             }
           }
           double inn[4];
+#pragma unroll
           for (int q = 0; q < 4; ++q) inn[q] = z[q] - m[q];
           // NC = P - (G^T S) G, row by row in place of P (row r reads only P row r)
+#pragma unroll
           for (int r = 0; r < 8; ++r) {
             double acc = 0.0;
+#pragma unroll
             for (int k = 0; k < 4; ++k) acc = acc + G[8 * k + r] * inn[k];
             mean_out[8LL * i + r] = m[r] + acc;
             double KS[4];
+#pragma unroll
             for (int k = 0; k < 4; ++k) {
               double s2 = 0.0;
+#pragma unroll
               for (int q = 0; q < 4; ++q) s2 = s2 + G[8 * q + r] * S[4 * q + k];
               KS[k] = s2;
             }
+#pragma unroll
             for (int k = 0; k < 8; ++k) {
               double a2 = 0.0;
+#pragma unroll
               for (int q = 0; q < 4; ++q) a2 = a2 + KS[q] * G[8 * q + k];
               c[8 * r + k] = c[8 * r + k] - a2;
             }
           }
+          // symmetrise in place: (a + b) / 2 is symmetric in a and b
+#pragma unroll
           for (int r = 0; r < 8; ++r)
-            for (int k = 0; k < 8; ++k) o[8 * r + k] = (c[8 * r + k] + c[8 * k + r]) / 2.0;
+#pragma unroll
+            for (int k = r; k < 8; ++k) {
+              const double a = (c[8 * r + k] + c[8 * k + r]) / 2.0;
+              c[8 * r + k] = a;
+              c[8 * k + r] = a;
+            }
         }
       }
     }
     status[i] = st;
   }
   __syncthreads();
+  const double* OUT = op == 3 ? TA : TB;              // update writes its result over P
   for (int x = tid; x < nb * out_w; x += kKfBlock) {
     const int r = x / out_w, q = x - r * out_w;
-    cov_out[static_cast<long long>(i0) * out_w + x] = TB[r * kKfPad + q];
+    cov_out[static_cast<long long>(i0) * out_w + x] = OUT[r * kKfPad + q];
   }
 }
 
@@ -3071,7 +3099,7 @@ cudaError_t launch_kalman(int op, int n, const Params& P, const double* mi, cons
     kalman_predict_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, P, mi, ci, mo, co, status);
     return cudaGetLastError();
   }
-  const size_t smem = 2 * sizeof(double) * kKfBlock * kKfPad;
+  const size_t smem = (op == 3 ? 1 : 2) * sizeof(double) * kKfBlock * kKfPad;
   cudaFuncSetAttribute(kalman_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   kalman_kernel<<<(n + kKfBlock - 1) / kKfBlock, kKfBlock, smem, st>>>(op, n, P, mi, ci, z, mo, co, status);
   return cudaGetLastError();
