@@ -2372,10 +2372,12 @@ __device__ void mm8(const double* A, const double* B, double* C, bool bt) {
 }
 
 // The KalmanFilter batch API on dense 8x8 states. A 64-thread block stages
-// its 64 covariances (and the outputs) through shared memory with coalesced
-// 16-byte-per-thread copies (rows padded to 65 doubles against bank
-// conflicts); each thread then runs the reference's matrix expressions for
-// its state on its shared-memory rows, in the reference's operation order.
+// its 64 covariances through shared memory (rows padded to 65 doubles against
+// bank conflicts, every 8-byte piece in flight at once by cp.async); each
+// thread then runs the reference's matrix expressions for its state on its
+// shared-memory row, in the reference's operation order, with fully unrolled
+// (register-indexed) loops. Predict and update write their result over P, so
+// they need one tile (more blocks per SM); initiate / project use a second.
 constexpr int kKfBlock = 64, kKfPad = 65;
 __device__ __forceinline__ double kf_F(int r, int k) { return (k == r || (r < 4 && k == r + 4)) ? 1.0 : 0.0; }
 
@@ -2430,38 +2432,63 @@ __global__ void __launch_bounds__(kKfBlock) kalman_kernel(int op, int n, Params 
         for (int k = 0; k < 8; ++k) acc = acc + kf_F(r, k) * m[k];
         mean_out[8LL * i + r] = acc;
       }
-      // FP = F P (into o), R = FP F^T (into c). With finite inputs the zero
-      // terms of the dense products add exact zeros, so only the two nonzero
-      // terms are summed (same single rounding); otherwise the dense sums run
-      // as mm8 computes them (0 * inf = NaN must propagate like the reference's).
+      // F P then (F P) F^T, in place on the state's shared row. With finite
+      // inputs the zero terms of the dense products add exact zeros, so only
+      // the two nonzero terms are summed (same single rounding); otherwise
+      // the dense sums run as mm8 computes them (0 * inf = NaN must propagate
+      // like the reference's), one column / row at a time.
       bool finite = true;
+#pragma unroll
       for (int q = 0; q < 64; ++q) finite = finite && isfinite(c[q]);
       if (finite) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) c[8 * r + j] = c[8 * r + j] + c[8 * (r + 4) + j];
+#pragma unroll
         for (int r = 0; r < 8; ++r)
-          for (int j = 0; j < 8; ++j) o[8 * r + j] = r < 4 ? c[8 * r + j] + c[8 * (r + 4) + j] : c[8 * r + j];
-        for (int r = 0; r < 8; ++r)
-          for (int j = 0; j < 8; ++j) c[8 * r + j] = j < 4 ? o[8 * r + j] + o[8 * r + j + 4] : o[8 * r + j];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) c[8 * r + j] = c[8 * r + j] + c[8 * r + j + 4];
       } else {
-        for (int r = 0; r < 8; ++r)
-          for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < 8; ++j) {
+          double col[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
             double acc = 0.0;
+#pragma unroll
             for (int k = 0; k < 8; ++k) acc = acc + kf_F(r, k) * c[8 * k + j];
-            o[8 * r + j] = acc;
+            col[r] = acc;
           }
-        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int r = 0; r < 8; ++r) c[8 * r + j] = col[r];
+        }
+        for (int r = 0; r < 8; ++r) {
+          double row[8];
+#pragma unroll
           for (int j = 0; j < 8; ++j) {
             double acc = 0.0;
-            for (int k = 0; k < 8; ++k) acc = acc + o[8 * r + k] * kf_F(j, k);
-            c[8 * r + j] = acc;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc = acc + c[8 * r + k] * kf_F(j, k);
+            row[j] = acc;
           }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) c[8 * r + j] = row[j];
+        }
       }
+#pragma unroll
       for (int q = 0; q < 4; ++q) {
         double sp = KF::qpos(P, q, h), sv = KF::qvel(P, q, h);
         c[9 * q] = c[9 * q] + sp * sp;
         c[9 * (q + 4)] = c[9 * (q + 4)] + sv * sv;
       }
+#pragma unroll
       for (int r = 0; r < 8; ++r)
-        for (int k = 0; k < 8; ++k) o[8 * r + k] = (c[8 * r + k] + c[8 * k + r]) / 2.0;
+#pragma unroll
+        for (int k = r; k < 8; ++k) {
+          const double a = (c[8 * r + k] + c[8 * k + r]) / 2.0;
+          c[8 * r + k] = a;
+          c[8 * k + r] = a;
+        }
     } else {
       const double h = m[3];
       double S[16], Lc[16] = {0};
@@ -2559,112 +2586,11 @@ __global__ void __launch_bounds__(kKfBlock) kalman_kernel(int op, int n, Params 
     status[i] = st;
   }
   __syncthreads();
-  const double* OUT = op == 3 ? TA : TB;              // update writes its result over P
+  const double* OUT = (op == 1 || op == 3) ? TA : TB;   // predict / update write their result over P
   for (int x = tid; x < nb * out_w; x += kKfBlock) {
     const int r = x / out_w, q = x - r * out_w;
     cov_out[static_cast<long long>(i0) * out_w + x] = OUT[r * kKfPad + q];
   }
-}
-
-// Predict (op 1) of the batch API, one state per thread held in registers:
-// 16-byte loads of the thread's 512-byte covariance (L1 merges a warp's rows),
-// the same expressions as kalman_kernel's predict (finite inputs: the two
-// nonzero terms of F P and (F P) F^T; otherwise the dense sums), symmetrised
-// in place ((a + b) / 2 is symmetric in a and b).
-__global__ void __launch_bounds__(128) kalman_predict_kernel(int n, Params P, const double* mean_in,
-                                                             const double* cov_in, double* mean_out,
-                                                             double* cov_out, int* status) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double c[64];
-  const double2* src = reinterpret_cast<const double2*>(cov_in + 64LL * i);
-#pragma unroll
-  for (int q = 0; q < 32; ++q) {
-    const double2 v = src[q];
-    c[2 * q] = v.x;
-    c[2 * q + 1] = v.y;
-  }
-  double m[8];
-  const double2* msrc = reinterpret_cast<const double2*>(mean_in + 8LL * i);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const double2 v = msrc[q];
-    m[2 * q] = v.x;
-    m[2 * q + 1] = v.y;
-  }
-  const double h = m[3];
-  double mo[8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc = acc + kf_F(r, k) * m[k];
-    mo[r] = acc;
-  }
-  bool finite = true;
-#pragma unroll
-  for (int q = 0; q < 64; ++q) finite = finite && isfinite(c[q]);
-  if (finite) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) c[8 * r + j] = c[8 * r + j] + c[8 * (r + 4) + j];
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) c[8 * r + j] = c[8 * r + j] + c[8 * r + j + 4];
-  } else {
-    // dense sums (0 * inf = NaN propagates as in the reference), one column
-    // of F P at a time so everything stays in registers
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      double col[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc = acc + kf_F(r, k) * c[8 * k + j];
-        col[r] = acc;
-      }
-#pragma unroll
-      for (int r = 0; r < 8; ++r) c[8 * r + j] = col[r];
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      double row[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc = acc + c[8 * r + k] * kf_F(j, k);
-        row[j] = acc;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) c[8 * r + j] = row[j];
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const double sp = KF::qpos(P, q, h), sv = KF::qvel(P, q, h);
-    c[9 * q] = c[9 * q] + sp * sp;
-    c[9 * (q + 4)] = c[9 * (q + 4)] + sv * sv;
-  }
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (k >= r) {
-        const double a = (c[8 * r + k] + c[8 * k + r]) / 2.0;
-        c[8 * r + k] = a;
-        c[8 * k + r] = a;
-      }
-  double2* dst = reinterpret_cast<double2*>(cov_out + 64LL * i);
-#pragma unroll
-  for (int q = 0; q < 32; ++q) dst[q] = make_double2(c[2 * q], c[2 * q + 1]);
-  double2* mdst = reinterpret_cast<double2*>(mean_out + 8LL * i);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) mdst[q] = make_double2(mo[2 * q], mo[2 * q + 1]);
-  status[i] = 0;
 }
 
 __global__ void gating_kernel(int nt, const double* means, const double* covs, int nm, const double* z,
@@ -3093,13 +3019,7 @@ cudaError_t launch_lap_dense(int n, const int* shapes, const long long* cost_off
 cudaError_t launch_kalman(int op, int n, const Params& P, const double* mi, const double* ci, const double* z,
                           double* mo, double* co, int* status, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  if (op == 1 && !getenv("TF_KF_TILED") && (reinterpret_cast<uintptr_t>(mi) & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(ci) & 15) == 0 && (reinterpret_cast<uintptr_t>(mo) & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(co) & 15) == 0) {
-    kalman_predict_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, P, mi, ci, mo, co, status);
-    return cudaGetLastError();
-  }
-  const size_t smem = (op == 3 ? 1 : 2) * sizeof(double) * kKfBlock * kKfPad;
+  const size_t smem = ((op == 1 || op == 3) ? 1 : 2) * sizeof(double) * kKfBlock * kKfPad;
   cudaFuncSetAttribute(kalman_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   kalman_kernel<<<(n + kKfBlock - 1) / kKfBlock, kKfBlock, smem, st>>>(op, n, P, mi, ci, z, mo, co, status);
   return cudaGetLastError();
