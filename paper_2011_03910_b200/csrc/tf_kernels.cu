@@ -22,6 +22,17 @@
 
 namespace cg = cooperative_groups;
 
+#ifdef TF_BOUNDS
+#include <cstdio>
+#define TF_BCHK(cond, ...)                     \
+  do {                                         \
+    if (!(cond)) printf("TFBOUND " __VA_ARGS__); \
+  } while (0)
+#else
+#define TF_BCHK(cond, ...) \
+  do {                     \
+  } while (0)
+#endif
 namespace tfd {
 
 // Host-side launch helpers: the dynamic shared-memory opt-in of a kernel is
@@ -211,8 +222,11 @@ __device__ int gather_normalize(const T* src, long long stride, int dim, int qua
 // (each CTA's own latency matters), 256 when frames outnumber the SMs (more
 // CTAs per SM overlap one another's scan / NMS / gather phases): B200, cfg1
 // 32 frames 46 -> 39 us, cfg4 4,096 frames 0.71 -> 0.63 ms.
+#ifndef TF_FRAME_MINB
+#define TF_FRAME_MINB 4   // 256-thread CTAs: <= 64 registers, 4 CTAs per SM (cfg4: 5 -> 0.58 ms with spills, 1 -> 90 registers, 0.88 ms)
+#endif
 template <typename T, int kThreads>
-__global__ void __launch_bounds__(kThreads) frame_heads_kernel(FrameArgs a, Params P) {
+__global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1) frame_heads_kernel(FrameArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
   // With few frames a thread-block cluster scans each frame: every CTA takes a
   // share of the anchor groups and stores its ballots into the leader CTA's
@@ -791,6 +805,8 @@ __device__ __noinline__ void birth_rows(const float* dets, float* pool, const in
     const int r = d_pos[k];
     if (r < 0) continue;
     const float* src = dets + static_cast<long long>(k) * D;
+    TF_BCHK(nf - 1 - r >= 0 && (unsigned)f_stk[nf - 1 - r] < 1024u, "birth_rows blk %d nf %d r %d slot %d\n",
+            blockIdx.x, nf, r, nf - 1 - r >= 0 ? f_stk[nf - 1 - r] : -999);
     float* dst = pool + static_cast<long long>(f_stk[nf - 1 - r]) * D;
     if (D == 512) {
       float4 x[4];
@@ -867,6 +883,8 @@ __device__ __forceinline__ double cost_rounds(const CostView v, int worker, int 
     for (int j = 0; j < NB; ++j) {
       k[j] = __shfl_sync(FULL, idx, j);
       sl[j] = __shfl_sync(FULL, idx, NB + j);
+      TF_BCHK((unsigned)sl[j] < 1024u && (unsigned)k[j] < 1024u, "cost blk %d e %d sl %d k %d\n", blockIdx.x,
+              e0 + j, sl[j], k[j]);
     }
     double acc[NB];
 #pragma unroll
@@ -958,6 +976,7 @@ __device__ void ema_work(const EmaView v) {
     if (lane == 0) sl = v.slot[k];           // one remote load, broadcast
     sl = __shfl_sync(FULL, sl, 0);
     if (sl < 0) continue;
+    TF_BCHK((unsigned)sl < 1024u, "ema blk %d k %d sl %d\n", blockIdx.x, k, sl);
     float* te = v.pool + static_cast<long long>(sl) * v.D;
     const float* de = v.dets + static_cast<long long>(k) * v.D;
     if (v.D == 512) {                                   // one pass, rows held in registers
@@ -1332,6 +1351,8 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     }
     const int K = frame_count(b);
     T = s_T;
+    TF_BCHK(tid != 0 || (T + s_nfree == Tm && T <= Tm && K <= Km), "frame blk %d b %d T %d nfree %d Tm %d K %d\n",
+            blockIdx.x, b, T, s_nfree, Tm, K);
     if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; s_Efr = 0; t_frame0 = clock64(); }
     // this frame's detections were prefetched (this thread's copies land here;
     // the predict barrier publishes all of them); start the next frame's
