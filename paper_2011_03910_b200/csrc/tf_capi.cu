@@ -345,6 +345,8 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
     delete c;
     return TF_ARGUMENT;
   }
+  // (TF_CAP_ENTRIES lowers the on-chip entry capacity: tests of the global-pool path)
+  if (const char* ce = getenv("TF_CAP_ENTRIES")) entries = std::max(16, std::min(entries, atoi(ce)));
   c->cap_entries = entries;
   cudaError_t e = cudaSuccess;
   auto A = [&](auto** p, size_t n) {

@@ -207,6 +207,20 @@ def test_narrow_association_ctas_match_oracle(monkeypatch):
     assert cmp.frames == 6 * 24
 
 
+@pytest.mark.parametrize("cluster,narrow", [("16", False), ("1", False), ("1", True)])
+def test_pooled_entries_path_matches_oracle(monkeypatch, cluster, narrow):
+    """Frames whose gated entries exceed the on-chip capacity keep them in the
+    stream's global pool; forced here with a tiny capacity, for the cluster,
+    single-CTA and 128-thread associations."""
+    monkeypatch.setenv("TF_CAP_ENTRIES", "64")
+    monkeypatch.setenv("TF_CLUSTER", cluster)
+    if narrow:
+        monkeypatch.setenv("TF_ASSOC_NARROW", "1")
+    cmp = _run_parity("cfg1", steps=2, B=8, max_tracks=160, max_detections=96,
+                      expect_threads=128 if narrow else 256)
+    assert cmp.frames == 16
+
+
 def test_narrow_and_wide_association_agree(monkeypatch):
     """128- and 256-thread association CTAs give identical records and traces."""
     p, synth = _pkg()
