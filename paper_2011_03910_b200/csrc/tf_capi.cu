@@ -334,8 +334,9 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   if (getenv("TF_ASSOC_NARROW") && !getenv("TF_ASSOC_WIDE") &&
       assoc_smem_bytes(k.max_tracks, k.max_detections, 1024) + assoc_static <= half) {
     c->assoc_threads = kAssocThreadsSmall;
-    while (entries > 1024 && assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + assoc_static > half)
-      entries -= 128;
+    while (!getenv("TF_ASSOC_NARROW_SOLO") && entries > 1024 &&
+           assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + assoc_static > half)
+      entries -= 128;   // (TF_ASSOC_NARROW_SOLO keeps the full plan: one 128-thread CTA per SM, diagnostics)
   }
   while (entries > 64 &&
          assoc_smem_bytes(k.max_tracks, k.max_detections, entries) + assoc_static > static_cast<size_t>(smem_optin))
