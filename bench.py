@@ -330,7 +330,10 @@ def run_ours(args):
 
     # kernel events in the timed region; the in-kernel phase timers (level 2)
     # only in the separate diagnostic pass below (streamed runs keep them on)
-    lib.tf_set_profiling(eng.ctx, 2 if streamed else 1)
+    # events on every prof_stride-th update: their host cost would otherwise
+    # show in small-batch runs (B = 1: ~6 event records per 30 us update)
+    prof_stride = max(1, 8 // B)
+    lib.tf_set_profiling(eng.ctx, (2 if streamed else 1) | (prof_stride << 4))
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ms = 0.0
     barrier()
@@ -392,7 +395,7 @@ def run_ours(args):
         hout = bt2.host_output(F)
         bt2.update(host_batches[0], host_out=hout)            # warm-up (allocates staging)
         barrier()
-        lib.tf_set_profiling(bt2.engine.ctx, 1)
+        lib.tf_set_profiling(bt2.engine.ctx, 1 | (prof_stride << 4))
         e_start.record(stream)
         for i in range(1, 1 + e2e_steps):
             bt2.update(host_batches[i], host_out=hout, sync=False)
@@ -494,6 +497,7 @@ def run_ours(args):
                          "ms_per_launch": assoc_launch_ms if dominant == "associate_kernel" else frame_launch_ms,
                          "note": "association is a per-stream dependency chain (latency-bound); DESIGN.md s6"},
             "kernels": {
+                "event_sample_stride": prof_stride,   # CUDA events on every N-th timed update
                 "frame_heads_kernel": {"ms_per_launch": frame_launch_ms, "bytes_per_launch": frame_bytes_launch,
                                        "GBps": f_gbs, "frac": f_gbs / peak},
                 "associate_kernel": {"ms_per_launch": assoc_launch_ms, "bytes_per_launch": assoc_bytes_launch,

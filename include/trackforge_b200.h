@@ -223,7 +223,8 @@ int tf_export_tracks(tf_ctx* ctx, int32_t stream, tf_track_export* out, void* cu
 /* Optional CUDA-event timing of the two kernels of every update (bench.py).
  * enabled: 0 off, 1 kernel events, 2 kernel events + the association
  * kernel's in-kernel phase timers (tf_phase_stats; they cost ~1% of the
- * kernel, so timed runs use 1). tf_kernel_times synchronises, returns the
+ * kernel, so timed runs use 1); enabled | (N << 4) records the events on
+ * every N-th update only (their host cost shows at small batches). tf_kernel_times synchronises, returns the
  * summed milliseconds of frame_heads_kernel and associate_kernel over the
  * updates since the last call, and resets the accumulators. */
 int tf_set_profiling(tf_ctx* ctx, int32_t enabled);

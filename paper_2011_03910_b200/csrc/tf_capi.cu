@@ -74,7 +74,10 @@ struct tf_ctx {
   // streams touched by the last update (for tf_finish)
   int last_begin, last_count;
   // optional per-kernel CUDA-event timing (bench.py roofline)
-  int profiling;
+  int profiling;                 // bit 0 kernel events, bit 1 in-kernel phase timers
+  int prof_stride = 1;            // events on every prof_stride-th update
+  long long prof_counter = 0;
+  bool prof_on = true;            // events for the current update
   std::vector<cudaEvent_t> events;   // triples: before frame kernel, after it, after associate
   size_t events_used;
   double last_h2d_ms;              // host->device copy time of the last tf_kernel_times window
@@ -236,7 +239,7 @@ cudaError_t upload_frame_index(tf_ctx* c, long long* dst, const long long* src, 
 }
 
 cudaError_t prof_mark(tf_ctx* c, int which, cudaStream_t st) {
-  if (!c->profiling) return cudaSuccess;
+  if (!c->profiling || !c->prof_on) return cudaSuccess;
   const size_t idx = c->events_used + which;
   while (c->events.size() <= idx) {
     cudaEvent_t e;
@@ -497,6 +500,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     rc = check_ordering(c, stream_begin + ls, reinterpret_cast<const long long*>(frame_index) + static_cast<size_t>(ls) * B, B);
     if (rc) return rc;
   }
+  c->prof_on = c->profiling && (c->prof_counter++ % c->prof_stride) == 0;
   TF_CUDA(c, cudaSetDevice(c->device));
   // buffer set and streams: without pipelining everything runs on `st` with set 0;
   // with pipelining the decode of this update (on `st`) overlaps the previous
@@ -697,6 +701,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
     if (rc) return rc;
   }
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  c->prof_on = c->profiling && (c->prof_counter++ % c->prof_stride) == 0;
   TF_CUDA(c, cudaSetDevice(c->device));
   for (int b = 0; b < 2; ++b)
     if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
@@ -887,7 +892,10 @@ int tf_export_tracks(tf_ctx* c, int32_t stream, tf_track_export* o, void* cuda_s
 
 int tf_set_profiling(tf_ctx* c, int32_t enabled) {
   if (!c) return TF_ARGUMENT;
-  c->profiling = enabled;
+  c->profiling = enabled & 15;
+  c->prof_stride = enabled >> 4 > 0 ? enabled >> 4 : 1;
+  c->prof_counter = 0;
+  c->prof_on = true;
   c->events_used = 0;
   TF_CUDA(c, cudaMemset(c->d_stats, 0, 32 * sizeof(long long)));
   return TF_OK;
