@@ -22,8 +22,8 @@
 
 namespace cg = cooperative_groups;
 
-#ifdef TF_BOUNDS
 #include <cstdio>
+#ifdef TF_BOUNDS
 #define TF_BCHK(cond, ...)                     \
   do {                                         \
     if (!(cond)) printf("TFBOUND " __VA_ARGS__); \
@@ -1180,7 +1180,22 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     s_ph[(i)] += now_ - t_sub;                        \
     t_sub = now_;                                     \
   }
+#ifdef TF_CANARY
+  // debug: 64 words past the plan, checked at every phase mark (smem overrun hunt)
+  unsigned* const canary = reinterpret_cast<unsigned*>(smem + pl.total);
+  for (int x = tid; x < 64; x += blockDim.x) canary[x] = 0xC0FFEE00u + x;
+#define TF_CANARY_CHECK(i)                                                                          \
+  if (tid == 0)                                                                                     \
+    for (int x_ = 0; x_ < 64; ++x_)                                                                 \
+      if (canary[x_] != 0xC0FFEE00u + x_) {                                                         \
+        printf("TFCANARY blk %d frame %d mark %d word %d val %08x\n", blockIdx.x, b, (i), x_, canary[x_]); \
+        canary[x_] = 0xC0FFEE00u + x_;                                                              \
+      }
+#else
+#define TF_CANARY_CHECK(i)
+#endif
 #define TF_MARK(i)                                    \
+  TF_CANARY_CHECK(i)                                  \
   if (a.stats && tid == 0) {                          \
     const long long now_ = clock64();                 \
     if ((i) > 0) s_ph[(i)] += now_ - t_mark;          \
@@ -2235,6 +2250,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     }
     __syncthreads();
     TF_SUB(30);
+    TF_CANARY_CHECK(30);
     if (s_err != STATUS_CLEAR) {
       if (tid == 0) s_status = (b << 8) | (s_err & 0xff);
       break;
@@ -2938,7 +2954,11 @@ cudaError_t launch_frame_rows(const double* boxes, const double* obj, const floa
 
 template <bool kExt>
 static cudaError_t launch_associate_t(const AssocArgs& a, int n_streams, const Params& P, cudaStream_t st) {
+#ifdef TF_CANARY
+  const size_t smem = assoc_smem_bytes(a.cap_tracks, a.cap_det, a.cap_entries) + 256;
+#else
   const size_t smem = assoc_smem_bytes(a.cap_tracks, a.cap_det, a.cap_entries);
+#endif
   if (a.threads == kAssocThreadsSmall) {
     set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreadsSmall, kExt>), smem);
     associate_kernel<kAssocThreadsSmall, kExt><<<n_streams, kAssocThreadsSmall, smem, st>>>(a, P);
