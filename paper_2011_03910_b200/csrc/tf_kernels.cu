@@ -1167,7 +1167,8 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   __shared__ int s_warp[33];
   __shared__ unsigned long long s_scan64[33];
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_Efr;
-  __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2, s_nlive[2], s_nmulti;   // the follower-applied EMA of frame s_ema_b
+  __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2, s_nlive[2], s_nmulti;
+  __shared__ int s_cflag;   // component labelling (its own flag: threads may still be reading peeling's last s_flag)   // the follower-applied EMA of frame s_ema_b
   int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
   int* f_stk = reinterpret_cast<int*>(smem + pl.off_fstk);
 
@@ -1803,13 +1804,13 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
           c_nc[x] = 0;
           c_ne[x] = 0;
         }
-        if (tid == 0) s_flag = 1;
+        if (tid == 0) s_cflag = 1;
         for (;;) {
           __syncthreads();
-          const int go = s_flag;
+          const int go = s_cflag;
           __syncthreads();
           if (!go) break;
-          if (tid == 0) s_flag = 0;
+          if (tid == 0) s_cflag = 0;
           __syncthreads();
           for (int q = tid; q < E_live; q += blockDim.x) {
             const int e = c_elist[q];
@@ -1819,7 +1820,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
               const int m = min(la, lb);
               atomicMin(&c_lab[r], m);
               atomicMin(&c_lab[c], m);
-              s_flag = 1;
+              s_cflag = 1;
             }
           }
           __syncthreads();
@@ -2145,6 +2146,9 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     }
     const long long fR = static_cast<long long>(f) * a.out.max_records;
     const int base_free = s_nfree;
+    // read before the compaction's barriers: tid 0 updates s_next at the end
+    // of its birth loop, possibly before a slow warp reaches the birth block
+    const long long next_id = s_next;
     // matched records, trace, free-stack pushes, then the ordered in-place
     // compaction one chunk of blockDim rows per round: destinations never
     // exceed sources, and a round's reads finish before its writes
@@ -2199,7 +2203,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     // birth (lane 0 initialises the row, the warp copies the embedding)
     {
       const int nf = base_free + n_rm;
-      const long long next = s_next;
+      const long long next = next_id;
       TF_MARK(7);
       birth_rows(a.det.emb + fK * static_cast<long long>(D), a.trk.emb_pool + sT * static_cast<long long>(D), d_pos,
                  f_stk, nf, K, D);
