@@ -246,7 +246,7 @@ def tracking_quality(args, cfg_name, S, B, cap, dev, steps=8):
 
     gen = synth.make(cfg_name, device=dev, seed=args.seed + 1000, streams=S)
     gen.record_truth()
-    bt = p.BatchTracker(S, frames_per_update=B, capacity=cap)
+    bt = p.BatchTracker(S, tracker_config(args), frames_per_update=B, capacity=cap)
     outs = []
     for i in range(steps):
         batch = gen.next_batch(B)
@@ -258,6 +258,14 @@ def tracking_quality(args, cfg_name, S, B, cap, dev, steps=8):
     rep = moteval.evaluate(gen.truth_frames(0), moteval.outputs_to_frames(outs))
     return {"stream": 0, "frames": len(outs), "iou_min": 0.5, "MOTA": rep.mota, "IDF1": rep.idf1,
             "MOTP": rep.motp, "IDs": rep.id_switches, "FP": rep.fp, "FN": rep.fn, "scorer": "GPU moteval"}
+
+
+def tracker_config(args):
+    """TrackerConfig of the run: the reference path, or the JDE extensions (--jde)."""
+    import paper_2011_03910_b200 as p
+    if getattr(args, "jde", False):
+        return p.TrackerConfig(motion_lambda=0.98, iou_stage=True, iou_threshold=0.5)
+    return p.TrackerConfig()
 
 
 def run_ours(args):
@@ -304,7 +312,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     pipe = not (streamed or args.no_pipeline)
-    bt = p.BatchTracker(S, frames_per_update=B, capacity=cap, pipeline=pipe)
+    bt = p.BatchTracker(S, tracker_config(args), frames_per_update=B, capacity=cap, pipeline=pipe)
     eng, lib = bt.engine, bt.engine.lib
     stream = torch.cuda.current_stream()
 
@@ -318,7 +326,7 @@ def run_ours(args):
     cand = kept = recs = 0
     if not streamed:
         # counts for the algorithmic bytes: one traced pass on a twin tracker
-        twin = p.BatchTracker(S, frames_per_update=B, capacity=cap)
+        twin = p.BatchTracker(S, tracker_config(args), frames_per_update=B, capacity=cap)
         for i in range(W + K):
             r = twin.update(batches[i], trace=True)
             if i >= W:
@@ -370,7 +378,7 @@ def run_ours(args):
     if not streamed:
         # per-phase breakdown of the association: the same batches on a fresh
         # tracker with the phase timers on, outside the timed region
-        pbt = p.BatchTracker(S, frames_per_update=B, capacity=cap, pipeline=pipe)
+        pbt = p.BatchTracker(S, tracker_config(args), frames_per_update=B, capacity=cap, pipeline=pipe)
         lib.tf_set_profiling(pbt.engine.ctx, 2)
         for i in range(W + K):
             pbt.update(batches[i], trace=False, sync=False)
@@ -391,7 +399,7 @@ def run_ours(args):
             tuple(h.cpu().pin_memory() for h in batches[i].heads),
             tuple(e.cpu().contiguous(memory_format=torch.channels_last).pin_memory() for e in batches[i].embs))
             for i in range(1 + e2e_steps)]
-        bt2 = p.BatchTracker(S, frames_per_update=B, capacity=cap, pipeline=pipe)
+        bt2 = p.BatchTracker(S, tracker_config(args), frames_per_update=B, capacity=cap, pipeline=pipe)
         hout = bt2.host_output(F)
         bt2.update(host_batches[0], host_out=hout)            # warm-up (allocates staging)
         barrier()
@@ -482,7 +490,8 @@ def run_ours(args):
                        "generation": "streamed between steps, steps timed one by one" if streamed
                        else "pre-generated on device",
                        "pipeline": "decode of step i+1 overlaps association of step i" if pipe else "off",
-                       "parallelism": f"streams sharded over {world} rank(s), final NCCL all_gather"},
+                       "parallelism": f"streams sharded over {world} rank(s), final NCCL all_gather",
+                       "tracker": "jde-extensions (lambda 0.98, IoU stage 0.5)" if args.jde else "reference"},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps if e2e_ms else 0,
                     "kernels": e2e_kernels,
@@ -544,6 +553,8 @@ def main():
     ap.add_argument("--ref-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="serialise decode and association")
+    ap.add_argument("--jde", action="store_true",
+                    help="JDE extensions on (lambda = 0.98 fused cost, IoU second stage at 0.5); off = reference path")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f16"],
                     help="head / embedding input type (f16 = MIXED-precision input mode, SURVEY 8(f))")
     args = ap.parse_args()
