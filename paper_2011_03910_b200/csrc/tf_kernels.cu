@@ -23,6 +23,15 @@
 namespace cg = cooperative_groups;
 
 #include <cstdio>
+// Debug: extra CTA barriers at the transitions selected by TF_XSYNC_MASK
+// (race bisection; compiled out by default).
+#ifndef TF_XSYNC_MASK
+#define TF_XSYNC_MASK 0
+#endif
+#define TF_XSYNC(n)                                   \
+  do {                                                \
+    if ((TF_XSYNC_MASK >> (n)) & 1) __syncthreads();  \
+  } while (0)
 #ifdef TF_BOUNDS
 #define TF_BCHK(cond, ...)                     \
   do {                                         \
@@ -1369,6 +1378,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     T = s_T;
     TF_BCHK(tid != 0 || (T + s_nfree == Tm && T <= Tm && K <= Km), "frame blk %d b %d T %d nfree %d Tm %d K %d\n",
             blockIdx.x, b, T, s_nfree, Tm, K);
+    TF_XSYNC(0);
     if (tid == 0) { s_err = STATUS_CLEAR; s_amp = 0.0; s_Efr = 0; t_frame0 = clock64(); }
     // this frame's detections were prefetched (this thread's copies land here;
     // the predict barrier publishes all of them); start the next frame's
@@ -1560,6 +1570,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
                         nw * C);
       __syncthreads();
     }
+    TF_XSYNC(1);
     // the previous frame's EMA list was consumed before S1: reset it
     for (int k = tid; k < K; k += blockDim.x) ema_slot[k] = -1;
     if (wid == 0) {                       // amplitude of the finite costs (read by the LAP after barriers)
@@ -1570,6 +1581,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
       if (lane == 0) s_amp = m;
     }
+    TF_XSYNC(2);
     TF_MARK(3);
     // errors from here on finish the frame's cluster barriers, then stop
     const bool frame_ok = (s_err == STATUS_CLEAR) && (s_ema_err == STATUS_CLEAR);
@@ -1612,6 +1624,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       // until peeling ends.)
       // (plain selects of shared pointers, not pointer arrays: the compiler then
       // keeps them in the shared window -- LDS / ATOMS instead of generic ops)
+      TF_XSYNC(3);
       unsigned* const km0 = reinterpret_cast<unsigned*>(p_cmin);
       unsigned* const km1 = km0 + K;
       unsigned* const rk0 = reinterpret_cast<unsigned*>(p_rmin);
@@ -1706,6 +1719,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
         __syncthreads();
         if (!*flag) break;
       }
+      TF_XSYNC(4);
       TF_SUB(17);
       // residual edges: the last peeling round's list
       const int E_live = huge ? 0 : s_nlive[last_round & 1];
@@ -2009,6 +2023,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     // ---- matches + max_cost threshold (tf/assoc.py:77-107), then the
     // matched tracks' Kalman update + lifecycle (tf/tracker.py:114-143), one
     // thread per track in one pass; matched tracks also post their EMA work
+    TF_XSYNC(5);
     TF_MARK(5);
     if (kExt && P.iou_stage) {
       // JDE extension: first-stage matches, then the IoU stage on what is left
@@ -2144,6 +2159,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       if (tid == 0) s_status = (b << 8) | TF_CAPACITY;
       break;
     }
+    TF_XSYNC(6);
     const long long fR = static_cast<long long>(f) * a.out.max_records;
     const int base_free = s_nfree;
     // read before the compaction's barriers: tid 0 updates s_next at the end
@@ -2204,6 +2220,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     {
       const int nf = base_free + n_rm;
       const long long next = next_id;
+      TF_XSYNC(7);
       TF_MARK(7);
       birth_rows(a.det.emb + fK * static_cast<long long>(D), a.trk.emb_pool + sT * static_cast<long long>(D), d_pos,
                  f_stk, nf, K, D);
