@@ -1609,7 +1609,6 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       const int NN = T + K;
       for (int r = tid; r < T; r += blockDim.x) { rcol[r] = -1; p_ra[r] = 1; }
       for (int c = tid; c < K; c += blockDim.x) { p_ca[c] = 1; c_map[c] = -1; }
-      unsigned long long* p_rminb = reinterpret_cast<unsigned long long*>(p_rmin);
       // edge ids are int16 in the peeling lists: beyond that, solve the padded matrix
       const bool huge = E > 32767;
       // Aggregates use 32-bit keys (the high word of the non-negative cost's
