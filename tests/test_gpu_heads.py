@@ -336,3 +336,22 @@ def test_fp16_layout_errors():
     bt = p.BatchTracker(1, frames_per_update=2)
     with pytest.raises(p.LayoutError):
         bt.update(mixed)
+
+
+def test_profiling_event_stride():
+    """tf_set_profiling(level | stride << 4) records kernel events on every
+    stride-th update only (bench.py samples them at small batches)."""
+    import ctypes as C
+    p, synth = _pkg()
+    gen = synth.make("cfg0", device="cuda", seed=3)
+    bt = p.BatchTracker(1, frames_per_update=1)
+    lib = bt.engine.lib
+    lib.tf_set_profiling(bt.engine.ctx, 1 | (4 << 4))
+    for _ in range(8):
+        bt.update(gen.next_batch(1), sync=False)
+    bt.join()
+    fr, asc, n = C.c_double(), C.c_double(), C.c_int64()
+    lib.tf_kernel_times(bt.engine.ctx, C.byref(fr), C.byref(asc), C.byref(n))
+    lib.tf_set_profiling(bt.engine.ctx, 0)
+    assert n.value == 2 and fr.value > 0 and asc.value > 0
+    assert _launch_info(bt)[0] == 256
