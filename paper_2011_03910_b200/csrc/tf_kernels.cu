@@ -842,7 +842,11 @@ __device__ __noinline__ void birth_rows(const float* dets, float* pool, const in
 // the leader's wait ends when the last cost lands, without a release fence.
 
 // pairs per warp per round (one L2 round trip per frame where possible)
-__device__ __forceinline__ int cost_nb(int E, int n_workers) { return E > 2 * n_workers ? 4 : 2; }
+// (3 pairs when that still fits one round: more warps share a frame's
+// entries; cfg1 cost phase 4.16 -> 3.98 us)
+__device__ __forceinline__ int cost_nb(int E, int n_workers) {
+  return E > 3 * n_workers ? 4 : E > 2 * n_workers ? 3 : 2;
+}
 
 // entries of a frame costed by follower warps (workers >= lead_workers)
 __device__ __forceinline__ int follower_entries(int E, int n_workers, int lead_workers) {
@@ -953,7 +957,10 @@ __device__ __noinline__ void cost_work(const CostView v, int worker, int n_worke
   // (worker = global warp index): no atomics on the critical path. Up to
   // 4 pairs per warp per round (4 x 2 rows x 2 KB of 128-bit loads in flight)
   // so a frame's entries take one round trip to L2 where possible.
-  const double amp = cost_nb(v.E, n_workers) == 4 ? cost_rounds<4>(v, worker, n_workers) : cost_rounds<2>(v, worker, n_workers);
+  const int nb = cost_nb(v.E, n_workers);
+  const double amp = nb == 4   ? cost_rounds<4>(v, worker, n_workers)
+                     : nb == 3 ? cost_rounds<3>(v, worker, n_workers)
+                               : cost_rounds<2>(v, worker, n_workers);
   // amplitude = max |finite| (tf/assoc.py:71): one slot per worker, reduced
   // by the leader (a contended u64 atomicMax over DSMEM is a CAS loop)
   if (lane_id() == 0) {
