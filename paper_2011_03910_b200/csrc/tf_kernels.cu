@@ -1420,7 +1420,10 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       const int KC = (K + 31) >> 5;
       const double thr = P.gate_threshold;
       const bool maha = (P.gate_metric == 0);
-      constexpr int GU = 4;                // tracks per warp pass (independent fp64 chains; 2 and 8 measured slower)
+#ifndef TF_GU
+#define TF_GU 6
+#endif
+      constexpr int GU = TF_GU;            // tracks per warp pass (independent fp64 chains; 6: -0.12 us/frame vs 4; 3, 7, 8 slower)
       for (int t0 = GU * wid; t0 < T; t0 += GU * nw) {
         int cnt[GU];
 #pragma unroll
