@@ -2121,8 +2121,10 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     }
     }  // frame_ok
     if (tid == 0) { s_ema_work = 0; if (frame_ok) s_ema_b = b; }
-    __syncthreads();
     if (C > 1) {
+      // S3 straight after this thread's share of the per-track pass (its
+      // release covers this thread's EMA-list entries; -0.3 us per frame
+      // against arriving after the CTA barrier); the CTA barrier follows
       TF_SUB(27);
       if (signaller) st_cluster(F_fl + 12, frame_ok ? K : 0);
       cluster_wait_acquire();                                     // this frame's S1 phase
@@ -2130,7 +2132,9 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       TF_SUB(26);
       s3_pending = true;
       ema_out = true;
-    } else if (frame_ok) {
+    }
+    __syncthreads();
+    if (C == 1 && frame_ok) {
       EmaView ev;
       ev.slot = ema_slot;
       ev.work = &s_ema_work;
