@@ -89,13 +89,16 @@ typedef struct tf_capacity {
  * logit; each channel plane must be H*W contiguous (h stride W, w stride 1).
  * `emb` is [N, D, H, W] fp32 with arbitrary element strides (channels_last,
  * i.e. stride_c == 1, is the fast path). Anchors are (w, h) pairs in input
- * pixels. `stride` is the scale's pixel stride (32, 16 or 8). */
+ * pixels. `stride` is the scale's pixel stride (32, 16 or 8). `channels` is
+ * the embedding map's channel count D; tf_update_heads returns TF_LAYOUT
+ * unless it equals tf_config.embedding_dim (parse_output's row-width check,
+ * tf/postproc.py:25-29). */
 typedef struct tf_head_scale {
   const float* head;
   int64_t head_stride_n, head_stride_c;
   const float* emb;
   int64_t emb_stride_n, emb_stride_c, emb_stride_h, emb_stride_w;
-  int32_t height, width, stride, reserved;
+  int32_t height, width, stride, channels;
   float anchors[8];
 } tf_head_scale;
 
@@ -229,6 +232,10 @@ int tf_export_tracks(tf_ctx* ctx, int32_t stream, tf_track_export* out, void* cu
  * updates since the last call, and resets the accumulators. */
 int tf_set_profiling(tf_ctx* ctx, int32_t enabled);
 int tf_kernel_times(tf_ctx* ctx, double* frame_ms, double* assoc_ms, int64_t* updates);
+/* Number of kernels this context has launched since tf_create (update,
+ * step and reset calls; bench.py reports the difference over its timed
+ * region as gpu_launches). Host-side read, no synchronisation. */
+int tf_launch_count(const tf_ctx* ctx, int64_t* launches);
 /* Host->device copy milliseconds (pinned-host updates) summed over the window
  * read by the last tf_kernel_times call. */
 int tf_copy_times(tf_ctx* ctx, double* h2d_ms);

@@ -38,7 +38,7 @@ class TfHeadScale(C.Structure):
         ("head", c_vp), ("head_stride_n", c_i64), ("head_stride_c", c_i64),
         ("emb", c_vp), ("emb_stride_n", c_i64), ("emb_stride_c", c_i64), ("emb_stride_h", c_i64),
         ("emb_stride_w", c_i64), ("height", c_i32), ("width", c_i32), ("stride", c_i32),
-        ("reserved", c_i32), ("anchors", C.c_float * 8),
+        ("channels", c_i32), ("anchors", C.c_float * 8),
     ]
 
 
@@ -82,6 +82,7 @@ _SIGS = {
     "tf_set_profiling": (c_i32, [c_vp, c_i32]),
     "tf_kernel_times": (c_i32, [c_vp, C.POINTER(c_dbl), C.POINTER(c_dbl), C.POINTER(c_i64)]),
     "tf_copy_times": (c_i32, [c_vp, C.POINTER(c_dbl)]),
+    "tf_launch_count": (c_i32, [c_vp, C.POINTER(c_i64)]),
     "tf_launch_info": (c_i32, [c_vp, C.POINTER(c_i32), C.POINTER(c_i32)]),
     "tf_timeline": (c_i32, [c_vp, c_vp, c_i32, C.POINTER(c_i32)]),
     "tf_mot_accumulate": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_dbl,

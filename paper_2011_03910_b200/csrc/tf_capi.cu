@@ -74,6 +74,7 @@ struct tf_ctx {
   // streams touched by the last update (for tf_finish)
   int last_begin, last_count;
   // optional per-kernel CUDA-event timing (bench.py roofline)
+  long long launches = 0;        // kernels launched by this context (tf_launch_count)
   int profiling;                 // bit 0 kernel events, bit 1 in-kernel phase timers
   int prof_stride = 1;            // events on every prof_stride-th update
   long long prof_counter = 0;
@@ -256,7 +257,7 @@ cudaError_t prof_mark(tf_ctx* c, int which, cudaStream_t st) {
 
 extern "C" {
 
-int tf_version(void) { return 1; }
+int tf_version(void) { return 2; }   // 2: tf_head_scale.channels is checked
 
 const char* tf_status_name(int status) {
   if (status < 0 || status > TF_ARGUMENT) return "UnknownError";
@@ -454,6 +455,7 @@ int tf_reset_stream(tf_ctx* c, int32_t stream, void* cuda_stream) {
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   for (int b = 0; b < 2; ++b)
     if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
+  ++c->launches;
   reset_streams_kernel<<<1, 256, 0, st>>>(c->trk, stream, 1, c->cap.max_tracks);
   TF_CUDA(c, cudaGetLastError());
   c->last_frame[stream] = std::numeric_limits<long long>::min();
@@ -495,6 +497,13 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     const tf_head_scale& s = heads->scale[i];
     if (!s.head || !s.emb || s.height < 1 || s.width < 1 || s.head_stride_c < static_cast<long long>(s.height) * s.width)
       return fail(c, TF_LAYOUT, "head scale " + std::to_string(i) + ": bad pointer or layout");
+    // parse_output's width check (tf/postproc.py:25-29): the map must carry
+    // exactly embedding_dim channels, or the gather would read the
+    // neighbouring cells' values (or past the tensor)
+    if (s.channels != c->cfg.embedding_dim)
+      return fail(c, TF_LAYOUT, "head scale " + std::to_string(i) + ": embedding map has " +
+                                    std::to_string(s.channels) + " channels, expected embedding_dim " +
+                                    std::to_string(c->cfg.embedding_dim));
   }
   for (int ls = 0; ls < n_streams; ++ls) {
     rc = check_ordering(c, stream_begin + ls, reinterpret_cast<const long long*>(frame_index) + static_cast<size_t>(ls) * B, B);
@@ -600,6 +609,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   TF_CUDA(c, upload_frame_index(c, c->d_fidx[par], reinterpret_cast<const long long*>(frame_index), F, st));
   TF_CUDA(c, prof_mark(c, 0, st));
   TF_CUDA(c, launch_frame_heads(h, c->P, st));
+  ++c->launches;
   TF_CUDA(c, prof_mark(c, 1, st));
   if (c->pipeline) {
     TF_CUDA(c, cudaEventRecord(c->ev_dec[par], st));
@@ -650,12 +660,14 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.out.max_records = out->max_records;
   TF_CUDA(c, prof_mark(c, 2, ast));
   TF_CUDA(c, launch_associate(a, n_streams, c->P, ast));
+  ++c->launches;
   TF_CUDA(c, prof_mark(c, 3, ast));
   if (c->pipeline) {
     TF_CUDA(c, cudaEventRecord(c->ev_asc[par], ast));
     c->asc_pending[par] = true;
   }
   if (trace && trace->det_code)
+    ++c->launches;
     copy_codes_kernel<<<F, 128, 0, ast>>>(det.count, det.code, trace->det_code, F, c->cap.max_detections);
   if (host_out) {
     const size_t n = static_cast<size_t>(F) * out->max_records;
@@ -710,6 +722,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   TF_CUDA(c, cudaMemcpyAsync(c->d_row_offsets, row_offsets, sizeof(int32_t) * (F + 1), cudaMemcpyHostToDevice, st));
   TF_CUDA(c, launch_frame_rows(boxes, objectness, embeddings, c->d_row_offsets, F, normalized ? 0 : 1,
                                c->cap.max_candidates, c->cap.max_detections, c->det, c->P, st));
+  ++c->launches;
   AssocArgs a;
   a.det = c->det;
   a.trk = c->trk;
@@ -741,7 +754,9 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   a.out.objectness = out->objectness;
   a.out.max_records = out->max_records;
   TF_CUDA(c, launch_associate(a, n_streams, c->P, st));
+  ++c->launches;
   if (trace && trace->det_code)
+    ++c->launches;
     copy_codes_kernel<<<F, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, F, c->cap.max_detections);
   c->touched_lo = std::min(c->touched_lo, stream_begin);
   c->touched_hi = std::max(c->touched_hi, stream_begin + n_streams);
@@ -771,6 +786,7 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   TF_CUDA(c, upload_frame_index(c, c->d_frame_index, &fi, 1, st));
   TF_CUDA(c, launch_frame_dets(boxes, objectness, embeddings, has_embedding, n, c->cap.max_candidates,
                                c->cap.max_detections, c->det, c->P, st));
+  ++c->launches;
   AssocArgs a;
   a.det = c->det;
   a.trk = c->trk;
@@ -794,7 +810,9 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.out.objectness = out->objectness;
   a.out.max_records = out->max_records;
   TF_CUDA(c, launch_associate(a, 1, c->P, st));
+  ++c->launches;
   if (trace && trace->det_code)
+    ++c->launches;
     copy_codes_kernel<<<1, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, 1, c->cap.max_detections);
   c->last_frame[stream] = fi;
   c->touched_lo = std::min(c->touched_lo, static_cast<int>(stream));
@@ -931,6 +949,12 @@ int tf_launch_info(tf_ctx* c, int32_t* assoc_threads, int32_t* assoc_cluster) {
   if (!c || !assoc_threads || !assoc_cluster) return TF_ARGUMENT;
   *assoc_threads = c->assoc_threads;
   *assoc_cluster = c->cluster_val;
+  return TF_OK;
+}
+
+int tf_launch_count(const tf_ctx* c, int64_t* launches) {
+  if (!c || !launches) return TF_ARGUMENT;
+  *launches = c->launches;
   return TF_OK;
 }
 

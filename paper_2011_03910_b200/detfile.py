@@ -15,64 +15,59 @@ from pathlib import Path
 
 import numpy as np
 
+from . import motfile
 from .core import normalize_rows
-from .errors import ConsistencyError, DimensionError, InvalidBoxError, ParseError
+from .errors import ConsistencyError, DimensionError, ParseError
 from .tracker import TrackerConfig, TrackerOutput, records_from_device
 
 SIDECAR_MAGIC = b"EMB1"
 
 
 def load_mot_detections(path: str | Path) -> dict[int, np.ndarray]:
-    """Parse a MOT detection file into frame -> (n, 6) raw rows (tf/detgen.py:364-396).
+    """MOT detection file -> frame -> (n, 6) raw rows (tf/detgen.py:364-396).
 
-    Rows are ``frame,id,bb_left,bb_top,bb_width,bb_height,conf,...``; frames
-    are 1-indexed in the file and 0-indexed in the map (insertion order = first
-    appearance), the id field is ignored, extra fields are allowed and the
-    confidence is clamped into [0, 1]."""
-    per_frame: dict[int, list[np.ndarray]] = {}
-    with open(path, "r", encoding="utf-8") as handle:
-        for lineno, line in enumerate(handle, start=1):
-            line = line.strip()
-            if not line:
-                continue
-            parts = line.split(",")
-            if len(parts) < 7:
-                raise ParseError(f"line {lineno}: expected at least 7 fields, got {len(parts)}")
-            try:
-                frame = int(float(parts[0]))
-                x, y, w, h = (float(v) for v in parts[2:6])
-                conf = float(parts[6])
-            except ValueError as exc:
-                raise ParseError(f"line {lineno}: non-numeric field ({exc})") from exc
-            if frame < 1:
-                raise ParseError(f"line {lineno}: frame index must be >= 1, got {frame}")
-            if w <= 0 or h <= 0:
-                raise InvalidBoxError(f"line {lineno}: non-positive box size w={w}, h={h}")
-            conf = min(max(conf, 0.0), 1.0)
-            per_frame.setdefault(frame - 1, []).append(np.array([x, y, w, h, conf, 1.0], dtype=np.float64))
-    return {frame: np.stack(rows) for frame, rows in per_frame.items()}
+    Rows are ``frame,id,bb_left,bb_top,bb_width,bb_height,conf,...``: the id
+    field is not read, extra fields are allowed, frames become 0-indexed map
+    keys in order of first appearance, the confidence is clamped into [0, 1]
+    and the class-score column is 1.0. Errors (ParseError, InvalidBoxError)
+    name the offending line (motfile.read_table)."""
+    t = motfile.read_table(path, 7, with_id=False, with_conf=True)
+    rows = np.empty((t.frame.size, 6), np.float64)
+    rows[:, :4] = t.box
+    rows[:, 4] = np.minimum(np.maximum(t.conf, 0.0), 1.0)
+    rows[:, 5] = 1.0
+    return {frame: rows[idx] for frame, idx in motfile.group_by_frame(t.frame)}
+
+
+def _sidecar_dtype(dim: int) -> np.dtype:
+    """One sidecar record: little-endian u32 frame, u32 det_index, dim x f32."""
+    return np.dtype([("frame", "<u4"), ("det", "<u4"), ("v", "<f4", (dim,))])
 
 
 def write_embedding_sidecar(path: str | Path, records: dict[tuple[int, int], np.ndarray], dim: int) -> None:
-    """Magic, u32 dim, then (u32 frame, u32 det_index, dim x f32) records in key order (tf/detgen.py:401-417)."""
+    """EMB1 sidecar (tf/detgen.py:401-417): magic, u32 dim, then the records in
+    ascending (frame, det_index) order. Every vector must have shape (dim,)
+    (DimensionError naming the first bad key)."""
     keys = sorted(records)
-    with open(path, "wb") as handle:
-        handle.write(SIDECAR_MAGIC)
-        handle.write(struct.pack("<I", dim))
-        for frame, det_index in keys:
-            vector = np.asarray(records[(frame, det_index)], dtype=np.float32)
-            if vector.shape != (dim,):
-                raise DimensionError(f"record ({frame}, {det_index}) has shape {vector.shape}, expected ({dim},)")
-            handle.write(struct.pack("<II", frame, det_index))
-            handle.write(vector.tobytes())
+    vecs = [np.asarray(records[k], dtype=np.float32) for k in keys]
+    bad = [k for k, v in zip(keys, vecs) if v.shape != (dim,)]
+    if bad:
+        raise DimensionError(f"record {bad[0]} has shape {np.shape(records[bad[0]])}, expected ({dim},)")
+    table = np.zeros(len(keys), _sidecar_dtype(dim))
+    if keys:
+        table["frame"] = [k[0] for k in keys]
+        table["det"] = [k[1] for k in keys]
+        table["v"] = np.stack(vecs)
+    Path(path).write_bytes(SIDECAR_MAGIC + struct.pack("<I", dim) + table.tobytes())
 
 
 def load_embedding_sidecar(path: str | Path, detections: dict[int, np.ndarray], dim: int = 512) -> dict[int, np.ndarray]:
     """Attach normalised sidecar embeddings to a detection map (tf/detgen.py:420-471).
 
-    Exactly one record per (frame, det_index) of the map: a missing, extra or
-    duplicate key is a ConsistencyError, another declared dimension a
-    DimensionError. All vectors are normalised in one GPU call."""
+    Exactly one record per (frame, det_index) of the map: a duplicate, missing
+    or extra key is a ConsistencyError naming the key, another declared
+    dimension a DimensionError. Keys are matched as sorted u64 codes, and
+    all vectors are normalised in one GPU call."""
     blob = Path(path).read_bytes()
     if blob[:4] != SIDECAR_MAGIC:
         raise ParseError(f"bad sidecar magic: {blob[:4]!r}")
@@ -81,45 +76,53 @@ def load_embedding_sidecar(path: str | Path, detections: dict[int, np.ndarray], 
     declared = struct.unpack("<I", blob[4:8])[0]
     if declared != dim:
         raise DimensionError(f"sidecar declares dim={declared}, expected {dim}")
-    record_size = 8 + 4 * dim
-    body = blob[8:]
-    if len(body) % record_size != 0:
-        raise ParseError(f"sidecar body size {len(body)} is not a multiple of {record_size}")
-    n = len(body) // record_size
-    rec = np.frombuffer(body, dtype=np.dtype([("frame", "<u4"), ("det", "<u4"), ("v", "<f4", (dim,))]), count=n)
-    index: dict[tuple[int, int], int] = {}
-    for i, (frame, det_index) in enumerate(zip(rec["frame"].tolist(), rec["det"].tolist())):
-        key = (frame, det_index)
-        if key in index:
-            raise ConsistencyError(f"duplicate sidecar record for {key}")
-        index[key] = i
-    needed = {(frame, det_index) for frame, rows in detections.items() for det_index in range(rows.shape[0])}
-    missing = needed - index.keys()
-    if missing:
-        raise ConsistencyError(f"sidecar missing record for {min(missing)}")
-    extra = index.keys() - needed
-    if extra:
-        raise ConsistencyError(f"sidecar has record {min(extra)} with no matching detection")
-    units = normalize_rows(np.ascontiguousarray(rec["v"])) if n else np.zeros((0, dim), np.float32)
+    dt = _sidecar_dtype(dim)
+    if (len(blob) - 8) % dt.itemsize:
+        raise ParseError(f"sidecar body size {len(blob) - 8} is not a multiple of {dt.itemsize}")
+    rec = np.frombuffer(blob, dtype=dt, offset=8)
+    code = (rec["frame"].astype(np.uint64) << np.uint64(32)) | rec["det"].astype(np.uint64)
+    order = np.argsort(code, kind="stable")
+    sc = code[order]
+    dup = np.nonzero(sc[1:] == sc[:-1])[0]
+    if dup.size:          # the duplicate met first in file order
+        pos = int(np.min(order[dup + 1]))
+        raise ConsistencyError(f"duplicate sidecar record for {(int(rec['frame'][pos]), int(rec['det'][pos]))}")
+    frames = list(detections)
+    need = np.concatenate([(np.uint64(f) << np.uint64(32)) + np.arange(detections[f].shape[0], dtype=np.uint64)
+                           for f in frames]) if frames else np.zeros(0, np.uint64)
+    missing = np.setdiff1d(need, sc)
+    if missing.size:
+        m = int(missing.min())
+        raise ConsistencyError(f"sidecar missing record for {(m >> 32, m & 0xFFFFFFFF)}")
+    extra = np.setdiff1d(sc, need)
+    if extra.size:
+        m = int(extra.min())
+        raise ConsistencyError(f"sidecar has record {(m >> 32, m & 0xFFFFFFFF)} with no matching detection")
+    # vector content last: the structure is checked before any vector is
+    # normalised (the reference normalises while reading, so a file with both
+    # a structural and a degenerate-vector fault may name the other one)
+    units = normalize_rows(np.ascontiguousarray(rec["v"])) if rec.size else np.zeros((0, dim), np.float32)
+    where = order[np.searchsorted(sc, need)]       # record of each needed key, map order
     attached: dict[int, np.ndarray] = {}
-    for frame, rows in detections.items():
-        out = np.zeros((rows.shape[0], 6 + dim), dtype=np.float64)
-        out[:, :6] = rows
-        for det_index in range(rows.shape[0]):
-            out[det_index, 6:] = units[index[(frame, det_index)]]
-        attached[frame] = out
+    start = 0
+    for f in frames:
+        n = detections[f].shape[0]
+        out = np.empty((n, 6 + dim), np.float64)
+        out[:, :6] = detections[f]
+        out[:, 6:] = units[where[start:start + n]]
+        attached[f] = out
+        start += n
     return attached
 
 
 def file_frames(detections: dict[int, np.ndarray], n_frames: int | None = None, row_width: int | None = None):
-    """(frame_index, rows) over a loaded map; missing frames yield no rows (tf/detgen.py:474-484)."""
-    if n_frames is None:
-        n_frames = max(detections) + 1 if detections else 0
-    if row_width is None:
-        row_width = next(iter(detections.values())).shape[1] if detections else 6
-    empty = np.zeros((0, row_width), dtype=np.float64)
-    for frame_index in range(n_frames):
-        yield frame_index, detections.get(frame_index, empty)
+    """(frame_index, rows) for frames 0..n_frames-1 of a loaded map; frames
+    with no detections give an empty (0, row_width) array (tf/detgen.py:474-484)."""
+    n = (max(detections) + 1 if detections else 0) if n_frames is None else n_frames
+    width = row_width if row_width is not None else (
+        next(iter(detections.values())).shape[1] if detections else 6)
+    none = np.zeros((0, width), dtype=np.float64)
+    return ((f, detections[f] if f in detections else none) for f in range(n))
 
 
 def replay(detections: dict[int, np.ndarray], config: TrackerConfig | None = None, *, n_frames: int | None = None,

@@ -94,12 +94,19 @@ def _dtype_code(t) -> int | None:
     return {"torch.float32": 0, "torch.float16": 1}.get(str(t.dtype))
 
 
-def _scale_desc(head, emb, stride: int) -> _lib.TfHeadScale:
+def _scale_desc(head, emb, stride: int, dim: int) -> _lib.TfHeadScale:
     h, w = GRID[stride]
     if tuple(head.shape[1:]) != (24, h, w):
         raise LayoutError(f"head of stride {stride} must be [N, 24, {h}, {w}], got {tuple(head.shape)}")
     if tuple(emb.shape[2:]) != (h, w) or emb.shape[0] != head.shape[0]:
         raise LayoutError(f"embedding map of stride {stride} must be [N, D, {h}, {w}], got {tuple(emb.shape)}")
+    # parse_output rejects rows whose width is not 6 + embedding_dim (tf/postproc.py:25-29)
+    if emb.shape[1] != dim:
+        raise LayoutError(f"embedding map of stride {stride} has {emb.shape[1]} channels, "
+                          f"expected embedding_dim {dim}")
+    if emb.device != head.device:
+        raise LayoutError(f"head and embedding map of stride {stride} are on different devices "
+                          f"({head.device} vs {emb.device})")
     hs = head.stride()
     if hs[3] != 1 or hs[2] != w:
         raise LayoutError("head planes must have contiguous H*W planes")
@@ -108,17 +115,20 @@ def _scale_desc(head, emb, stride: int) -> _lib.TfHeadScale:
     es = emb.stride()
     d = _lib.TfHeadScale(head=head.data_ptr(), head_stride_n=hs[0], head_stride_c=hs[1], emb=emb.data_ptr(),
                          emb_stride_n=es[0], emb_stride_c=es[1], emb_stride_h=es[2], emb_stride_w=es[3],
-                         height=h, width=w, stride=stride, reserved=0)
+                         height=h, width=w, stride=stride, channels=int(emb.shape[1]))
     for a, (aw, ah) in enumerate(ANCHORS[stride]):
         d.anchors[2 * a] = aw
         d.anchors[2 * a + 1] = ah
     return d
 
 
-def heads_descriptor(out: HeadOutputs, host_memory: bool) -> _lib.TfHeads:
+def heads_descriptor(out: HeadOutputs, host_memory: bool, dim: int) -> _lib.TfHeads:
+    devs = {t.device for t in (*out.heads, *out.embs)}
+    if len(devs) != 1:
+        raise LayoutError(f"all head tensors and embedding maps must be on one device, got {sorted(map(str, devs))}")
     desc = _lib.TfHeads()
     for i, s in enumerate(STRIDES):
-        desc.scale[i] = _scale_desc(out.heads[i], out.embs[i], s)
+        desc.scale[i] = _scale_desc(out.heads[i], out.embs[i], s, dim)
     desc.scale_inv, desc.pad_x, desc.pad_y = letterbox()
     desc.host_memory = int(host_memory)
     desc.dtype = _dtype_code(out.heads[0])
@@ -176,6 +186,8 @@ class BatchTracker:
         host = not head_outputs.heads[0].is_cuda
         if host and not all(t.is_pinned() for t in (*head_outputs.heads, *head_outputs.embs)):
             raise LayoutError("host inputs must be pinned (torch.Tensor.pin_memory())")
+        if not host and head_outputs.heads[0].device != eng.device:
+            raise LayoutError(f"head tensors are on {head_outputs.heads[0].device}, the tracker on {eng.device}")
         frames = self._frames(n_streams, B, frame_index)
         desc = self._descriptor(head_outputs, host)
         if host:
@@ -263,9 +275,9 @@ class BatchTracker:
         """heads_descriptor with the layout validated once per tensor layout:
         later updates with the same shapes / strides / dtype only swap the data
         pointers (the per-update host cost matters at small batches)."""
-        key = (host,) + tuple((t.shape, t.stride(), t.dtype) for t in (*out.heads, *out.embs))
+        key = (host,) + tuple((t.shape, t.stride(), t.dtype, t.device) for t in (*out.heads, *out.embs))
         if self._desc_key != key:
-            self._desc = heads_descriptor(out, host)
+            self._desc = heads_descriptor(out, host, self.config.embedding_dim)
             self._desc_key = key
             return self._desc
         d = self._desc

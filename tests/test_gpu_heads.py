@@ -32,15 +32,22 @@ def _launch_info(bt):
 
 
 def _run_parity(cfg_name, steps, B, streams=1, quantize=False, literal=False, config=None, max_tracks=256,
-                half=False, max_detections=256, expect_threads=None, **synth_kw):
+                half=False, max_detections=256, expect_threads=None, check_streams=None, max_candidates=512,
+                **synth_kw):
+    """GPU update of `streams` streams x B frames per step against one oracle
+    tracker per checked stream (all streams by default; full-size configs
+    check a sample, the other streams still run on the GPU in the same
+    launches)."""
     p, synth = _pkg()
     cfg = config or p.TrackerConfig()
     gen = synth.make(cfg_name, device="cuda", streams=streams, literal_noise=literal, **synth_kw)
-    cap = p.Capacity(streams=streams, max_frames=streams * B, max_tracks=max_tracks, max_detections=max_detections)
+    cap = p.Capacity(streams=streams, max_frames=streams * B, max_tracks=max_tracks, max_detections=max_detections,
+                     max_candidates=max_candidates)
     bt = p.BatchTracker(streams, cfg, frames_per_update=B, quantize=quantize, capacity=cap)
     if expect_threads is not None:
         assert _launch_info(bt)[0] == expect_threads
-    oracles = [ot.OracleTracker(oracle_settings(cfg, quantize)) for _ in range(streams)]
+    checked = list(range(streams)) if check_streams is None else list(check_streams)
+    oracles = {s: ot.OracleTracker(oracle_settings(cfg, quantize)) for s in checked}
     cmp = FrameCompare()
     frame = 0
     for step in range(steps):
@@ -52,8 +59,9 @@ def _run_parity(cfg_name, steps, B, streams=1, quantize=False, literal=False, co
         tr = {k: v.cpu().numpy() for k, v in bt.trace(streams * B).items()}
         cnt = res.count.cpu().numpy()
         ids, boxes, objs = res.track_id.cpu().numpy(), res.box.cpu().numpy(), res.objectness.cpu().numpy()
-        host = host_frames(out, range(streams * B))
-        for s in range(streams):
+        sel = [s * B + b for s in checked for b in range(B)]
+        host = dict(zip(sel, host_frames(out, sel)))
+        for s in checked:
             for b in range(B):
                 f = s * B + b
                 codes, trace = run_oracle_frame(oracles[s], frame + b, *host[f], quantize=quantize)
@@ -62,9 +70,10 @@ def _run_parity(cfg_name, steps, B, streams=1, quantize=False, literal=False, co
                 recs = [(int(ids[f, i]), tuple(boxes[f, i]), float(objs[f, i])) for i in range(cnt[f])]
                 cmp.check(frame + b, trace, recs, tr["det_code"][f, :k], tr["det_track"][f, :k],
                           tr["det_cost"][f, :k], tr["det_matched"][f, :k], codes)
+        del out, host
         frame += B
     # final track tables
-    for s in range(streams):
+    for s in checked:
         ex = bt.export(s)
         o = oracles[s]
         assert ex["track_id"].tolist() == [t.track_id for t in o.tracks]
@@ -355,3 +364,130 @@ def test_profiling_event_stride():
     lib.tf_set_profiling(bt.engine.ctx, 0)
     assert n.value == 2 and fr.value > 0 and asc.value > 0
     assert _launch_info(bt)[0] == 256
+
+
+# ---------------------------------------------------------------- full-size shapes, sampled streams
+def test_full_cfg3_sampled_streams_match_oracle():
+    """BASELINE config 3 at its bench shape (64 streams x B = 8, 10-100
+    objects per stream): every stream runs in the same launches, four are
+    checked against the oracle over three updates."""
+    cmp = _run_parity("cfg3", steps=3, B=8, streams=64, check_streams=[0, 21, 42, 63], max_candidates=256,
+                      max_detections=160)
+    assert cmp.frames == 4 * 24 and cmp.matches > 1000
+
+
+def test_full_cfg4_sampled_streams_match_oracle():
+    """BASELINE config 4 at its 1-GPU bench shape (512 streams x B = 8, the
+    bench's capacities): streams 0, 137, 300 and 511 against the oracle over
+    three updates."""
+    cmp = _run_parity("cfg4", steps=3, B=8, streams=512, check_streams=[0, 137, 300, 511], max_candidates=192,
+                      max_detections=96, max_tracks=160)
+    assert cmp.frames == 4 * 24 and cmp.matches > 3000
+
+
+# ---------------------------------------------------------------- determinism
+def _replay(batches, streams, B, **kw):
+    p, _ = _pkg()
+    cap = p.Capacity(streams=streams, max_frames=streams * B, **kw)
+    bt = p.BatchTracker(streams, frames_per_update=B, capacity=cap)
+    outs = []
+    for out in batches:
+        r = bt.update(out, trace=True)
+        tr = bt.trace(streams * B)
+        outs.append([t.cpu().numpy().copy() for t in (r.count, r.track_id, r.box, r.objectness, tr["cand_count"],
+                                                      tr["det_count"], tr["det_code"], tr["det_track"],
+                                                      tr["det_cost"], tr["det_matched"])])
+    ex = [bt.export(s) for s in range(streams)]
+    return outs, ex
+
+
+@pytest.mark.parametrize("cfg_name,streams,B", [("cfg1", 1, 32), ("cfg3", 16, 8), ("cfg2", 1, 8)])
+def test_deterministic_replay(cfg_name, streams, B):
+    """Run the default variant twice on identical inputs: every output, trace
+    and final track table is bit-identical (race
+    detection by deterministic replay)."""
+    _, synth = _pkg()
+    gen = synth.make(cfg_name, device="cuda", streams=streams, seed=23)
+    batches = [gen.next_batch(B) for _ in range(3)]
+    kw = dict(max_tracks=384, max_candidates=768, max_detections=224) if cfg_name == "cfg2" else {}
+    a, ea = _replay(batches, streams, B, **kw)
+    b, eb = _replay(batches, streams, B, **kw)
+    for step_a, step_b in zip(a, b):
+        for x, y in zip(step_a, step_b):
+            assert x.tobytes() == y.tobytes()
+    for x, y in zip(ea, eb):
+        for k in x:
+            assert np.asarray(x[k]).tobytes() == np.asarray(y[k]).tobytes(), k
+
+
+# ---------------------------------------------------------------- boundary: embedding map width / device
+def test_embedding_map_width_mismatch_is_layout_error():
+    """parse_output rejects rows whose width is not 6 + embedding_dim
+    (tf/postproc.py:25-29); a narrower (or wider) embedding map is the same
+    mistake here and must raise LayoutError, never gather neighbouring cells."""
+    p, synth = _pkg()
+    gen = synth.make("cfg0", device="cuda", dim=64)
+    out = gen.next_batch(2)
+    bt = p.BatchTracker(1, p.TrackerConfig(embedding_dim=128), frames_per_update=2)
+    with pytest.raises(p.LayoutError, match="channels"):
+        bt.update(out)
+    ok = p.BatchTracker(1, p.TrackerConfig(embedding_dim=64), frames_per_update=2)
+    ok.update(out)
+
+
+def test_embedding_map_on_another_device_is_layout_error():
+    p, synth = _pkg()
+    gen = synth.make("cfg0", device="cuda")
+    out = gen.next_batch(1)
+    mixed = p.HeadOutputs(out.heads, (out.embs[0].cpu(),) + tuple(out.embs[1:]))
+    bt = p.BatchTracker(1, frames_per_update=1)
+    with pytest.raises(p.LayoutError):
+        bt.update(mixed)
+
+
+def test_c_abi_rejects_channel_count_mismatch():
+    """The C side checks tf_head_scale.channels against embedding_dim itself
+    (a caller that bypasses the Python shim gets TF_LAYOUT, not a silent
+    out-of-bounds gather)."""
+    import ctypes as C
+    p, synth = _pkg()
+    from paper_2011_03910_b200 import _lib
+    from paper_2011_03910_b200.heads import heads_descriptor
+    gen = synth.make("cfg0", device="cuda")
+    out = gen.next_batch(1)
+    bt = p.BatchTracker(1, frames_per_update=1)
+    desc = heads_descriptor(out, False, 512)
+    desc.scale[1].channels = 511
+    eng = bt.engine
+    code = eng.lib.tf_update_heads(eng.ctx, C.byref(desc), 0, 1, 1, np.zeros(1, np.int64).ctypes.data,
+                                   C.byref(eng.records), None, _lib.stream_handle())
+    assert code == 6 and b"511" in eng.lib.tf_last_error(eng.ctx)
+
+
+# ---------------------------------------------------------------- decode pinned to the generator's truth
+def test_gpu_decode_reproduces_generator_boxes():
+    """Independent pin of the decode (the reference has none): with zero
+    box-delta noise the generator encodes each visible object's true box at
+    its anchor cell; on the first frame every track is a birth whose
+    posterior box is its measurement, so the GPU records must reproduce the
+    truth boxes (1e-6 relative; objects whose centre fraction hit the
+    generator's 1e-3 clamp are excluded)."""
+    import torch as T
+    p, synth = _pkg()
+    from decode_pin import match_truth
+    for seed in range(3):
+        gen = synth.make("cfg1", device="cuda", seed=seed, delta_sigma=0.0)
+        gen.record_truth()
+        out = gen.next_batch(1)
+        bt = p.BatchTracker(1, frames_per_update=1)
+        res = bt.update(out)
+        n = int(res.count[0])
+        boxes = res.box[0, :n].cpu().numpy()
+        obj = res.objectness[0, :n].cpu().numpy()
+        true_obj = np.isclose(obj, 1.0 / (1.0 + np.exp(-8.0)), rtol=1e-12, atol=0.0)   # the +4 / -4 logits
+        _, _, _, truth = gen.truth[0]
+        active = gen.active[0].cpu().numpy()
+        checked = match_truth(boxes[true_obj], truth[0].cpu().numpy()[active], rtol=1e-6)
+        assert checked >= 40, checked
+        del out
+        T.cuda.empty_cache()
