@@ -47,10 +47,10 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
-    objs = []
-    for src in SOURCES:
+    extra = os.environ.get("TF_NVCC_EXTRA", "").split()     # experiment switches (-D...)
+
+    def compile_one(src: str) -> str:
         obj = CSRC / (Path(src).stem + ".o")
-        extra = os.environ.get("TF_NVCC_EXTRA", "").split()     # experiment switches (-D...)
         cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(ROOT / "include"), "-c", str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -58,7 +58,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose:
             sys.stderr.write(res.stderr)
         (CSRC / (Path(src).stem + ".ptxas.txt")).write_text(res.stderr)
-        objs.append(str(obj))
+        return str(obj)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(len(SOURCES)) as pool:      # the sources compile independently
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
            "-cudart", "static", "-Xcompiler", "-fPIC"]

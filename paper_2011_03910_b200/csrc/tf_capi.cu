@@ -666,9 +666,10 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     TF_CUDA(c, cudaEventRecord(c->ev_asc[par], ast));
     c->asc_pending[par] = true;
   }
-  if (trace && trace->det_code)
+  if (trace && trace->det_code) {
     ++c->launches;
     copy_codes_kernel<<<F, 128, 0, ast>>>(det.count, det.code, trace->det_code, F, c->cap.max_detections);
+  }
   if (host_out) {
     const size_t n = static_cast<size_t>(F) * out->max_records;
     if (!c->pipeline) TF_CUDA(c, cudaEventRecord(c->ev_asc[par], ast));
@@ -755,9 +756,10 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   a.out.max_records = out->max_records;
   TF_CUDA(c, launch_associate(a, n_streams, c->P, st));
   ++c->launches;
-  if (trace && trace->det_code)
+  if (trace && trace->det_code) {
     ++c->launches;
     copy_codes_kernel<<<F, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, F, c->cap.max_detections);
+  }
   c->touched_lo = std::min(c->touched_lo, stream_begin);
   c->touched_hi = std::max(c->touched_hi, stream_begin + n_streams);
   for (int ls = 0; ls < n_streams; ++ls)
@@ -811,9 +813,10 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.out.max_records = out->max_records;
   TF_CUDA(c, launch_associate(a, 1, c->P, st));
   ++c->launches;
-  if (trace && trace->det_code)
+  if (trace && trace->det_code) {
     ++c->launches;
     copy_codes_kernel<<<1, 128, 0, st>>>(c->det.count, c->det.code, trace->det_code, 1, c->cap.max_detections);
+  }
   c->last_frame[stream] = fi;
   c->touched_lo = std::min(c->touched_lo, static_cast<int>(stream));
   c->touched_hi = std::max(c->touched_hi, static_cast<int>(stream) + 1);
