@@ -680,6 +680,13 @@ __device__ inline void warp_lap_reg(int n, int nr, const Rows R, double sentinel
       if (i == cur) break;
     }
   }
+  // column duals for lap_unique (the shared-memory solver keeps them in s.v)
+#pragma unroll
+  for (int q = 0; q < RC; ++q) {
+    const int j = lane + 32 * q;
+    if (j < n) s.v[j] = v[q];
+  }
+  __syncwarp();
 }
 
 // Exact solver dispatch: register-resident for n <= 256, shared-memory otherwise.
@@ -691,6 +698,122 @@ __device__ inline void warp_lap_fast(int n, int nr, const Rows R, double sentine
   else if (n <= 128) warp_lap_reg<4>(n, nr, R, sentinel, s, n_proc);
   else if (n <= 256) warp_lap_reg<8>(n, nr, R, sentinel, s, n_proc);
   else warp_lap(n, nr, R, sentinel, s, n_proc);
+}
+
+// ---------------------------------------------------------------- uniqueness
+// Is the optimum just found by warp_lap on a component (rows 0..nr-1 all
+// processed, columns 0..nc-1, every non-entry cell = sentinel) the only one,
+// with a margin? Decides whether the component solve may stand for the
+// reference's solve of the whole padded matrix: with a unique optimum (no
+// other matching of the component's finite edges within eps of its cost)
+// scipy, whose roundoff is far below eps, returns the same finite pairs
+// whatever its processing order. Equal costs alone do not decide it either
+// way (a 2 x 2 component with a + d == b + c and four distinct costs has two
+// optima, while equal costs on edges that never compete leave the optimum
+// unique), so the test runs on the solver's duals:
+//
+// with reduced costs r = c - u_i - v_j >= 0 (tight on the matching), any
+// other row-perfect matching M' costs sum_{M'} r more, plus -v_c0 when it
+// frees the matched column c0 of its start row (v <= 0, and 0 on free
+// columns). So near-optima are exactly the alternating cycles / paths of
+// cells with r <= eps, paths to a free column starting at a row whose column
+// has v >= -eps. Directed graph on rows: i -> mate(j) for every cell (i, j),
+// j != col(i), with r <= eps (sentinel cells too: r = sentinel - u_i - v_j,
+// which never holds for an entry cell since r >= 0), i -> FREE when j is
+// unmatched. An alternative changes the FINITE pairs (what the reference
+// reports) iff it uses an entry cell or moves a row matched by an entry
+// cell; cycles / paths made of sentinel cells only just permute padding.
+// One warp, lane = row; nr, nc <= 32 (larger components return false: the
+// caller then solves the whole padded matrix in the reference's order).
+template <class Rows>
+__device__ inline bool lap_unique(int nr, int nc, const Rows R, double sentinel, double eps, LapScratch s) {
+  if (nr > 32 || nc > 32) return false;
+  const int lane = lane_id();
+  if (lane < nc) s.row4col[lane] = -1;
+  __syncwarp();
+  const int ci = lane < nr ? s.col4row[lane] : -1;
+  if (lane < nr && ci >= 0 && ci < nc) s.row4col[ci] = static_cast<int16_t>(lane);
+  __syncwarp();
+  const double vj = lane < nc ? s.v[lane] : 0.0;
+  const int mate = lane < nc ? s.row4col[lane] : -1;
+  const unsigned matched_cols = __ballot_sync(FULL, lane < nc && mate >= 0);
+  const double ui = lane < nr ? s.u[lane] : 0.0;
+  // near-tight sentinel cells of row `lane`
+  unsigned smask = 0u;
+  const double theta = sentinel - ui - eps;
+  for (int j = 0; j < nc; ++j) {
+    const double v = __shfl_sync(FULL, vj, j);
+    if (lane < nr && j != ci && v >= theta) smask |= 1u << j;
+  }
+  // near-tight entry cells; is the row matched by an entry?
+  unsigned fmask = 0u, emask = 0u;
+  bool fm = false;
+  if (lane < nr) {
+    for (int e = R.begin(lane); e < R.end(lane); ++e) {
+      const int j = R.col(e);
+      if (j < 0 || j >= nc) continue;
+      emask |= 1u << j;
+      if (j == ci) {
+        fm = true;
+        continue;
+      }
+      if (R.val(e) - ui - s.v[j] <= eps) fmask |= 1u << j;
+    }
+    smask &= ~emask;          // an entry cell's cost is its entry, never the sentinel
+  }
+  // arcs to rows (via each column's mate) and to FREE
+  unsigned A = 0u, FA = 0u;
+  for (unsigned m = smask | fmask; m; m &= m - 1u) {
+    const int j = __ffs(m) - 1;
+    const int r = s.row4col[j];
+    if (r >= 0) {
+      A |= 1u << r;
+      if ((fmask >> j) & 1u) FA |= 1u << r;
+    }
+  }
+  const bool to_free = ((smask | fmask) & ~matched_cols) != 0u;
+  const bool ftofree = (fmask & ~matched_cols) != 0u;
+  // transitive closure by doubling: Rc = rows reachable in >= 1 arcs
+  unsigned Rc = A;
+  for (;;) {
+    unsigned nxt = Rc;
+    for (int k = 0; k < nr; ++k) {
+      const unsigned rk = __shfl_sync(FULL, Rc, k);
+      if ((Rc >> k) & 1u) nxt |= rk;
+    }
+    const bool changed = nxt != Rc;
+    Rc = nxt;
+    if (!__any_sync(FULL, changed)) break;
+  }
+  const unsigned tf_rows = __ballot_sync(FULL, lane < nr && to_free);
+  const bool free_reach = to_free || (Rc & tf_rows) != 0u;
+  // rows a path alternative may start from (their column's dual ~ 0), and
+  // everything they reach
+  const double vci = __shfl_sync(FULL, vj, ci > 0 ? ci & 31 : 0);   // every lane joins the shuffle
+  const bool freeable = lane < nr && ci >= 0 && ci < nc && vci >= -eps;
+  const unsigned fr_rows = __ballot_sync(FULL, freeable);
+  unsigned RF = fr_rows;
+  for (int k = 0; k < nr; ++k) {
+    const unsigned rk = __shfl_sync(FULL, Rc, k);
+    if ((fr_rows >> k) & 1u) RF |= rk;
+  }
+  const bool from_start = (RF >> lane) & 1u;
+  const unsigned fr_reach = __ballot_sync(FULL, lane < nr && free_reach);
+  bool alt = false;
+  if (lane < nr) {
+    if (fm && ((Rc >> lane) & 1u)) alt = true;                  // entry-matched row on a cycle
+    if (fm && from_start && free_reach) alt = true;             // ... on a path to a free column
+    if (ftofree && from_start) alt = true;                      // entry cell to a free column
+  }
+  // entry arcs lane -> k on a cycle (k reaches lane) or on a path (k reaches FREE)
+  for (int k = 0; k < nr; ++k) {
+    const unsigned rk = __shfl_sync(FULL, Rc, k);
+    if (lane < nr && ((FA >> k) & 1u)) {
+      if ((rk >> lane) & 1u) alt = true;
+      if (from_start && ((fr_reach >> k) & 1u)) alt = true;
+    }
+  }
+  return !__any_sync(FULL, alt);
 }
 
 }  // namespace tfd

@@ -1183,6 +1183,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   __shared__ int s_warp[33];
   __shared__ unsigned long long s_scan64[33];
   __shared__ int s_T, s_status, s_E, s_nfree, s_err, s_flag, s_tie, s_Efr;
+  __shared__ int s_alt;     // a component solve found a near-optimum (written only after every thread read s_tie)
   __shared__ int s_ema_work, s_ema_err, s_ema_b, s_flag2, s_nlive[2], s_nmulti;
   __shared__ int s_cflag;   // component labelling (its own flag: threads may still be reading peeling's last s_flag)   // the follower-applied EMA of frame s_ema_b
   int* ema_slot = reinterpret_cast<int*>(smem + pl.off_emas);
@@ -1719,8 +1720,11 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
           const int e = lst[q];
           const int r = erow[e], c = ecol[e];
           const unsigned key = static_cast<unsigned>(__double_as_longlong(eval[e]) >> 32);
-          if (key == km[c]) atomicAdd(&cc[c], 1);
-          if (key == rk[r]) atomicAdd(&rc[r], 1);
+          // counts of keys within one unit of the minimum: a forced pair must
+          // beat every rival by >= 2^-20 relative, far beyond any roundoff in
+          // the reference's solve (closer rivals stay for the exact residual)
+          if (key <= km[c] + 1u) atomicAdd(&cc[c], 1);
+          if (key <= rk[r] + 1u) atomicAdd(&rc[r], 1);
         }
         __syncthreads();
         int* flag = cur ? &s_flag2 : &s_flag;
@@ -1760,7 +1764,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
         c_elist = c_epos;
         c_epos = tmp;
       }
-      if (tid == 0) { s_tie = huge; s_nmulti = -1; }
+      if (tid == 0) { s_tie = huge; s_alt = 0; s_nmulti = -1; }
       if (!huge && E_live <= 32) {
         // Small residual (the common case): one warp labels the components,
         // checks them for equal costs and lays out the per-component problems;
@@ -1768,12 +1772,10 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
         if (wid == 0) {
           const bool on = lane < E_live;
           int r = 0, cn = 0, root = 0;
-          double v0 = 0.0;
           if (on) {
             const int e = c_elist[lane];
             r = erow[e];
             cn = T + ecol[e];
-            v0 = eval[e];
           }
           for (;;) {
             bool changed = false;
@@ -1797,13 +1799,6 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
             if (!__any_sync(FULL, changed)) break;
           }
           if (on) root = c_lab[r];
-          // equal costs inside one component -> the exact full restatement:
-          // lanes with equal cost bits (zeros unified) that share a root
-          const unsigned long long vkey =
-              on ? (v0 == 0.0 ? 0ull : static_cast<unsigned long long>(__double_as_longlong(v0))) : ~0ull - lane;
-          const unsigned same_v = __match_any_sync(FULL, vkey);
-          const unsigned same_r = __match_any_sync(FULL, on ? root : -1 - lane);
-          const bool tie = __any_sync(FULL, on && __popc(same_v & same_r) > 1);
           // distinct rows / columns / roots: the last writer of a marker owns it
           int* mark = c_lrp;
           if (on) { mark[r] = lane; mark[cn] = lane; }
@@ -1837,7 +1832,6 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
             c_eoff[i] = ine - vne;
           }
           if (lane == 0) {
-            s_tie = tie;
             s_nmulti = n_multi;
             if (a.stats) s_ph[10] += n_multi;
           }
@@ -1879,33 +1873,14 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
           const bool alive = x < T ? p_ra[x] != 0 : p_ca[x - T] != 0;
           if (alive) atomicAdd(x < T ? &c_nr[c_lab[x]] : &c_nc[c_lab[x]], 1);
         }
-        for (int q = tid; q < E_live; q += blockDim.x) {
-          const int e = c_elist[q];
-          const int root = c_lab[erow[e]];
-          atomicAdd(&c_ne[root], 1);
-          const double v0 = eval[e];
-          for (int q2 = q + 1; q2 < E_live && !s_tie; ++q2) {
-            const int e2 = c_elist[q2];
-            if (eval[e2] == v0 && c_lab[erow[e2]] == root) s_tie = 1;
-          }
-        }
+        for (int q = tid; q < E_live; q += blockDim.x) atomicAdd(&c_ne[c_lab[erow[c_elist[q]]]], 1);
         __syncthreads();
       }
       TF_SUB(16);
-      if (a.stats && tid == 0) { s_ph[8] += s_tie; s_ph[9] += E; s_ph[11] += 1; s_ph[12] += T; s_ph[13] += K; s_ph[14] += E_live; }
-      if (s_tie) {
-        if (wid == 0) {
-          const int n = T > K ? T : K;
-          const double sentinel = 2.0 * static_cast<double>(n) * fmax(s_amp, 1.0) + 1.0;
-          warp_lap_fast(n, T, CsrRows{rowptr, ecol, eval}, sentinel, L);
-          __syncwarp();
-          for (int r = lane; r < T; r += 32) {
-            const int c = L.col4row[r];
-            rcol[r] = static_cast<int16_t>(c < K ? c : -1);
-          }
-          TF_SUB(20);
-        }
-      } else {
+      // near-optimum margin of the component solves (costs are in [0, 2]
+      // scaled by the amplitude; the reference's roundoff is ~1e-13)
+      const double tie_eps = 1e-9 * fmax(1.0, s_amp);
+      if (!s_tie) {
         int n_multi = s_nmulti;
         const bool laid_out = n_multi >= 0;
         if (!laid_out) {
@@ -1964,7 +1939,16 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
               const int oe = __shfl_xor_sync(FULL, be, o);
               if (ob < best || (ob == best && oe > be)) { best = ob; be = oe; }
             }
+            // the optimum is unique iff no other edge comes within tie_eps
+            double second = INFINITY;
+            for (int q = lane; q < E_live; q += 32) {
+              const int e = c_elist[q];
+              if (e != be && c_lab[erow[e]] == root) second = fmin(second, eval[e]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) second = fmin(second, __shfl_xor_sync(FULL, second, o));
             if (lane == 0 && be >= 0) rcol[erow[be]] = ecol[be];
+            if (lane == 0 && !(second - best > tie_eps)) s_alt = 1;
             continue;
           }
           int nr_l = 0, nc_l = 0;
@@ -2026,6 +2010,9 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
             __syncwarp();
             warp_lap_fast(n_l, nc_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, Ls, nc_l);
             __syncwarp();
+            if (!lap_unique(nc_l, n_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, tie_eps, Ls) &&
+                lane == 0)
+              s_alt = 1;
             for (int j = lane; j < nc_l; j += 32) {
               const int lc = Ls.col4row[j];
               if (lc < nr_l) {
@@ -2037,6 +2024,9 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
           } else {
             warp_lap_fast(n_l, nr_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, Ls, nr_l);
             __syncwarp();
+            if (!lap_unique(nr_l, n_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, tie_eps,
+                            Ls) && lane == 0)
+              s_alt = 1;
             for (int r = lane; r < nr_l; r += 32) {
               const int j = Ls.col4row[r];
               if (j < nc_l) {
@@ -2047,10 +2037,28 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
             }
           }
         }
+        __syncthreads();
+        TF_SUB(19);
+      }
+      const bool full_solve = s_tie || s_alt;
+      if (a.stats && tid == 0) { s_ph[8] += full_solve; s_ph[9] += E; s_ph[11] += 1; s_ph[12] += T; s_ph[13] += K; s_ph[14] += E_live; }
+      if (full_solve) {
+        // a near-optimum exists (or the matrix is beyond the int16 edge
+        // lists): the whole padded matrix in the reference's order
+        if (wid == 0) {
+          const int n = T > K ? T : K;
+          const double sentinel = 2.0 * static_cast<double>(n) * fmax(s_amp, 1.0) + 1.0;
+          warp_lap_fast(n, T, CsrRows{rowptr, ecol, eval}, sentinel, L);
+          __syncwarp();
+          for (int r = lane; r < T; r += 32) {
+            const int c = L.col4row[r];
+            rcol[r] = static_cast<int16_t>(c < K ? c : -1);
+          }
+          TF_SUB(20);
+        }
       }
     }
     __syncthreads();
-    TF_SUB(19);
     TF_MARK(4);
     // ---- matches + max_cost threshold (tf/assoc.py:77-107), then the
     // matched tracks' Kalman update + lifecycle (tf/tracker.py:114-143), one
