@@ -627,6 +627,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
   a.threads = c->assoc_threads;
+  a.zero_smem = getenv("TF_ZERO_SMEM") != nullptr;
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
@@ -735,6 +736,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
   a.threads = c->assoc_threads;
+  a.zero_smem = getenv("TF_ZERO_SMEM") != nullptr;
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
@@ -800,6 +802,7 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
   a.threads = c->assoc_threads;
+  a.zero_smem = getenv("TF_ZERO_SMEM") != nullptr;
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;

@@ -723,61 +723,98 @@ __device__ inline void warp_lap_fast(int n, int nr, const Rows R, double sentine
 // unmatched. An alternative changes the FINITE pairs (what the reference
 // reports) iff it uses an entry cell or moves a row matched by an entry
 // cell; cycles / paths made of sentinel cells only just permute padding.
-// One warp, lane = row; nr, nc <= 32 (larger components return false: the
-// caller then solves the whole padded matrix in the reference's order).
+// Rows with no near-tight cell can neither move nor be displaced along an
+// alternative (a displaced row needs a cell of its own), so only the
+// "active" rows form the graph; it is solved by one warp with a lane per
+// active row (up to 32 of them, any component size; more active rows than
+// that return false and the caller solves the whole padded matrix in the
+// reference's order). A sentinel cell can be near-tight only for a row with
+// u >= sentinel - eps (v <= 0), and never on an entry (dual feasibility).
+template <class Rows>
+__device__ inline void lap_row_arcs(int i, int nc, const Rows R, double sentinel, double eps, LapScratch s,
+                                    const int16_t* act, unsigned& A, unsigned& FA, bool& to_free, bool& ftofree,
+                                    bool& fm) {
+  const int ci = s.col4row[i];
+  const double ui = s.u[i];
+  A = FA = 0u;
+  to_free = ftofree = fm = false;
+  for (int e = R.begin(i); e < R.end(i); ++e) {
+    const int j = R.col(e);
+    if (j < 0 || j >= nc) continue;
+    if (j == ci) {
+      fm = true;
+      continue;
+    }
+    if (R.val(e) - ui - s.v[j] <= eps) {
+      const int r = s.row4col[j];
+      if (r < 0) {
+        to_free = ftofree = true;
+      } else if (act == nullptr || act[r] >= 0) {
+        const unsigned bit = act ? 1u << act[r] : 1u;
+        A |= bit;
+        FA |= bit;
+      }
+    }
+  }
+  if (ui >= sentinel - eps) {
+    const double theta = sentinel - ui - eps;
+    for (int j = 0; j < nc; ++j) {
+      if (j == ci || s.v[j] < theta) continue;
+      const int r = s.row4col[j];
+      if (r < 0) to_free = true;
+      else if (act == nullptr || act[r] >= 0) A |= act ? 1u << act[r] : 1u;
+    }
+  }
+}
+
 template <class Rows>
 __device__ inline bool lap_unique(int nr, int nc, const Rows R, double sentinel, double eps, LapScratch s) {
-  if (nr > 32 || nc > 32) return false;
   const int lane = lane_id();
-  if (lane < nc) s.row4col[lane] = -1;
+  for (int j = lane; j < nc; j += 32) s.row4col[j] = -1;
   __syncwarp();
-  const int ci = lane < nr ? s.col4row[lane] : -1;
-  if (lane < nr && ci >= 0 && ci < nc) s.row4col[ci] = static_cast<int16_t>(lane);
-  __syncwarp();
-  const double vj = lane < nc ? s.v[lane] : 0.0;
-  const int mate = lane < nc ? s.row4col[lane] : -1;
-  const unsigned matched_cols = __ballot_sync(FULL, lane < nc && mate >= 0);
-  const double ui = lane < nr ? s.u[lane] : 0.0;
-  // near-tight sentinel cells of row `lane`
-  unsigned smask = 0u;
-  const double theta = sentinel - ui - eps;
-  for (int j = 0; j < nc; ++j) {
-    const double v = __shfl_sync(FULL, vj, j);
-    if (lane < nr && j != ci && v >= theta) smask |= 1u << j;
+  for (int i = lane; i < nr; i += 32) {
+    const int c = s.col4row[i];
+    if (c >= 0 && c < nc) s.row4col[c] = static_cast<int16_t>(i);
   }
-  // near-tight entry cells; is the row matched by an entry?
-  unsigned fmask = 0u, emask = 0u;
-  bool fm = false;
-  if (lane < nr) {
-    for (int e = R.begin(lane); e < R.end(lane); ++e) {
-      const int j = R.col(e);
-      if (j < 0 || j >= nc) continue;
-      emask |= 1u << j;
-      if (j == ci) {
-        fm = true;
-        continue;
-      }
-      if (R.val(e) - ui - s.v[j] <= eps) fmask |= 1u << j;
+  __syncwarp();
+  // active rows (a near-tight cell other than their own), numbered in row order
+  int16_t* act = s.rem;            // row -> active index or -1 (free scratch after the solve)
+  int16_t* row_of = s.path;        // active index -> row
+  int m = 0;
+  for (int i0 = 0; i0 < nr; i0 += 32) {
+    const int i = i0 + lane;
+    bool on = false;
+    if (i < nr) {
+      unsigned A, FA;
+      bool tf, ftf, fm;
+      lap_row_arcs(i, nc, R, sentinel, eps, s, nullptr, A, FA, tf, ftf, fm);
+      on = A != 0u || tf;
     }
-    smask &= ~emask;          // an entry cell's cost is its entry, never the sentinel
+    const unsigned bm = __ballot_sync(FULL, on);
+    if (i < nr) {
+      const int k = m + __popc(bm & ((1u << lane) - 1u));
+      act[i] = on && k < 32 ? static_cast<int16_t>(k) : static_cast<int16_t>(-1);
+      if (on && k < 32) row_of[k] = static_cast<int16_t>(i);
+    }
+    m += __popc(bm);
   }
-  // arcs to rows (via each column's mate) and to FREE
+  __syncwarp();
+  if (m == 0) return true;
+  if (m > 32) return false;
+  // the graph on the active rows: lane a = active row row_of[a]
   unsigned A = 0u, FA = 0u;
-  for (unsigned m = smask | fmask; m; m &= m - 1u) {
-    const int j = __ffs(m) - 1;
-    const int r = s.row4col[j];
-    if (r >= 0) {
-      A |= 1u << r;
-      if ((fmask >> j) & 1u) FA |= 1u << r;
-    }
+  bool to_free = false, ftofree = false, fm = false, freeable = false;
+  if (lane < m) {
+    const int i = row_of[lane];
+    lap_row_arcs(i, nc, R, sentinel, eps, s, act, A, FA, to_free, ftofree, fm);
+    const int ci = s.col4row[i];
+    freeable = ci >= 0 && ci < nc && s.v[ci] >= -eps;
   }
-  const bool to_free = ((smask | fmask) & ~matched_cols) != 0u;
-  const bool ftofree = (fmask & ~matched_cols) != 0u;
-  // transitive closure by doubling: Rc = rows reachable in >= 1 arcs
+  // transitive closure by doubling: Rc = active rows reachable in >= 1 arcs
   unsigned Rc = A;
   for (;;) {
     unsigned nxt = Rc;
-    for (int k = 0; k < nr; ++k) {
+    for (int k = 0; k < m; ++k) {
       const unsigned rk = __shfl_sync(FULL, Rc, k);
       if ((Rc >> k) & 1u) nxt |= rk;
     }
@@ -785,30 +822,28 @@ __device__ inline bool lap_unique(int nr, int nc, const Rows R, double sentinel,
     Rc = nxt;
     if (!__any_sync(FULL, changed)) break;
   }
-  const unsigned tf_rows = __ballot_sync(FULL, lane < nr && to_free);
+  const unsigned tf_rows = __ballot_sync(FULL, lane < m && to_free);
   const bool free_reach = to_free || (Rc & tf_rows) != 0u;
   // rows a path alternative may start from (their column's dual ~ 0), and
   // everything they reach
-  const double vci = __shfl_sync(FULL, vj, ci > 0 ? ci & 31 : 0);   // every lane joins the shuffle
-  const bool freeable = lane < nr && ci >= 0 && ci < nc && vci >= -eps;
-  const unsigned fr_rows = __ballot_sync(FULL, freeable);
+  const unsigned fr_rows = __ballot_sync(FULL, lane < m && freeable);
   unsigned RF = fr_rows;
-  for (int k = 0; k < nr; ++k) {
+  for (int k = 0; k < m; ++k) {
     const unsigned rk = __shfl_sync(FULL, Rc, k);
     if ((fr_rows >> k) & 1u) RF |= rk;
   }
   const bool from_start = (RF >> lane) & 1u;
-  const unsigned fr_reach = __ballot_sync(FULL, lane < nr && free_reach);
+  const unsigned fr_reach = __ballot_sync(FULL, lane < m && free_reach);
   bool alt = false;
-  if (lane < nr) {
+  if (lane < m) {
     if (fm && ((Rc >> lane) & 1u)) alt = true;                  // entry-matched row on a cycle
     if (fm && from_start && free_reach) alt = true;             // ... on a path to a free column
     if (ftofree && from_start) alt = true;                      // entry cell to a free column
   }
   // entry arcs lane -> k on a cycle (k reaches lane) or on a path (k reaches FREE)
-  for (int k = 0; k < nr; ++k) {
+  for (int k = 0; k < m; ++k) {
     const unsigned rk = __shfl_sync(FULL, Rc, k);
-    if (lane < nr && ((FA >> k) & 1u)) {
+    if (lane < m && ((FA >> k) & 1u)) {
       if ((rk >> lane) & 1u) alt = true;
       if (from_start && ((fr_reach >> k) & 1u)) alt = true;
     }

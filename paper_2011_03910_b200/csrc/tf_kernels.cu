@@ -1177,6 +1177,10 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   uint8_t* p_ca = smem + pl.off_pca;
   uint8_t* p_kr = smem + pl.off_pkr;
   uint8_t* p_kc = smem + pl.off_pkc;
+  if (a.zero_smem) {            // diagnostics: no byte of the plan keeps a previous CTA's value
+    for (size_t x = threadIdx.x; x < pl.total / 16; x += blockDim.x) reinterpret_cast<uint4*>(smem)[x] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+  }
   for (int x = threadIdx.x; x < Tm; x += blockDim.x) p_kr[x] = 0;
   for (int x = threadIdx.x; x < Km; x += blockDim.x) p_kc[x] = 0;
 

@@ -71,6 +71,7 @@ struct AssocArgs {
   long long* stats;              // [32] phase cycles / counters (nullptr = off)
   int cluster;                   // CTAs per stream (1 = no cluster)
   int threads;                   // kAssocThreads, or kAssocThreadsSmall (no cluster)
+  int zero_smem;                 // diagnostics (TF_ZERO_SMEM): clear the dynamic shared memory at launch
 };
 
 struct HeadLaunch {

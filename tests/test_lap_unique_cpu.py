@@ -62,40 +62,58 @@ def sap_rect(cost, n_proc):
     return col4row, np.array(u), np.array(v)
 
 
+def _row_arcs(i, cost, finite, col4row, row4col, u, v, sentinel, eps):
+    """Near-tight cells of row i other than its own: (target row or None for
+    a free column, is an entry cell); sentinel cells only when u_i >= sentinel - eps."""
+    nr, nc = cost.shape
+    out = []
+    for j in range(nc):
+        if j == col4row[i]:
+            continue
+        if finite[i, j]:
+            near = cost[i, j] - u[i] - v[j] <= eps
+        else:
+            near = u[i] >= sentinel - eps and v[j] >= sentinel - u[i] - eps
+        if near:
+            out.append((row4col[j] if row4col[j] >= 0 else None, bool(finite[i, j])))
+    return out
+
+
 def lap_unique(cost, finite, col4row, u, v, sentinel, eps):
-    """Python statement of the device's lap_unique (same graph, same rules)."""
+    """Python statement of the device's lap_unique (same active-row graph, same rules)."""
     nr, nc = cost.shape
     row4col = [-1] * nc
     for r, c in enumerate(col4row):
         row4col[c] = r
-    A, FA = [0] * nr, [0] * nr
-    to_free, ftofree, fm = [False] * nr, [False] * nr, [False] * nr
-    for i in range(nr):
-        fm[i] = bool(finite[i, col4row[i]])
-        for j in range(nc):
-            if j == col4row[i]:
-                continue
-            near = (cost[i, j] - u[i] - v[j] <= eps) if finite[i, j] else (v[j] >= sentinel - u[i] - eps)
-            if not near:
-                continue
-            if row4col[j] >= 0:
-                A[i] |= 1 << row4col[j]
-                if finite[i, j]:
-                    FA[i] |= 1 << row4col[j]
-            else:
-                to_free[i] = True
-                ftofree[i] = ftofree[i] or bool(finite[i, j])
+    arcs = [_row_arcs(i, cost, finite, col4row, row4col, u, v, sentinel, eps) for i in range(nr)]
+    active = [i for i in range(nr) if arcs[i]]
+    idx = {r: k for k, r in enumerate(active)}
+    m = len(active)
+    if m == 0:
+        return True
+    A, FA = [0] * m, [0] * m
+    to_free, ftofree, fm = [False] * m, [False] * m, [False] * m
+    for k, i in enumerate(active):
+        fm[k] = bool(finite[i, col4row[i]])
+        for tgt, fin in arcs[i]:
+            if tgt is None:
+                to_free[k] = True
+                ftofree[k] = ftofree[k] or fin
+            elif tgt in idx:
+                A[k] |= 1 << idx[tgt]
+                if fin:
+                    FA[k] |= 1 << idx[tgt]
     Rc = A[:]
     while True:
-        nxt = [Rc[i] | _or(Rc, Rc[i]) for i in range(nr)]
+        nxt = [Rc[i] | _or(Rc, Rc[i]) for i in range(m)]
         if nxt == Rc:
             break
         Rc = nxt
-    tf_rows = sum(1 << i for i in range(nr) if to_free[i])
-    free_reach = [to_free[i] or (Rc[i] & tf_rows) != 0 for i in range(nr)]
-    fr_rows = sum(1 << i for i in range(nr) if v[col4row[i]] >= -eps)
+    tf_rows = sum(1 << k for k in range(m) if to_free[k])
+    free_reach = [to_free[k] or (Rc[k] & tf_rows) != 0 for k in range(m)]
+    fr_rows = sum(1 << k for k, i in enumerate(active) if v[col4row[i]] >= -eps)
     RF = fr_rows | _or(Rc, fr_rows)
-    for i in range(nr):
+    for i in range(m):
         start = (RF >> i) & 1
         if fm[i] and (Rc[i] >> i) & 1:
             return False
@@ -103,7 +121,7 @@ def lap_unique(cost, finite, col4row, u, v, sentinel, eps):
             return False
         if ftofree[i] and start:
             return False
-        for k in range(nr):
+        for k in range(m):
             if (FA[i] >> k) & 1 and ((Rc[k] >> i) & 1 or (start and free_reach[k])):
                 return False
     return True
@@ -135,8 +153,8 @@ def test_lap_unique_matches_brute_force(seed):
     rng = np.random.default_rng(seed)
     agree = alternatives = 0
     for _ in range(400):
-        nr = int(rng.integers(1, 5))
-        nc = int(rng.integers(nr, 6))
+        nr = int(rng.integers(1, 6))
+        nc = int(rng.integers(nr, 7))
         finite = rng.random((nr, nc)) < rng.uniform(0.3, 0.9)
         # small integer costs: plenty of exact ties and equal sums (a + d == b + c)
         cost_f = rng.integers(0, 4, (nr, nc)).astype(np.float64) * 0.25
