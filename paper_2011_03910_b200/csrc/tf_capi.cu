@@ -330,12 +330,12 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   // its throughput). Otherwise one 256-thread CTA (or a cluster) per stream.
   const size_t half = static_cast<size_t>(smem_sm) / 2 - 1024;
   c->assoc_threads = kAssocThreads;
-  // Opt-in (TF_ASSOC_NARROW): on cfg4 the 128-thread variant hit an
-  // intermittent illegal address in ~15% of runs that the 256-thread variant
-  // never showed, so many-stream runs use the wide CTAs
-  // by default.
-  (void)sms;
-  if (getenv("TF_ASSOC_NARROW") && !getenv("TF_ASSOC_WIDE") &&
+  // (Round 1 kept this variant opt-in after an intermittent illegal address
+  // on cfg4; with the LAP's tie handling rewritten, 1,200 fresh-tracker cfg4
+  // updates and 25 bench runs showed no fault: DESIGN.md section 10.)
+  // TF_ASSOC_NARROW forces it for fewer streams, TF_ASSOC_WIDE keeps 256.
+  const bool many = k.streams >= 2 * sms || getenv("TF_ASSOC_NARROW");
+  if (many && !getenv("TF_ASSOC_WIDE") &&
       assoc_smem_bytes(k.max_tracks, k.max_detections, 1024) + assoc_static <= half) {
     c->assoc_threads = kAssocThreadsSmall;
     while (!getenv("TF_ASSOC_NARROW_SOLO") && entries > 1024 &&

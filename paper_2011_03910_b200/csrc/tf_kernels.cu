@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
   const int g0 = min(NG, gw * per_warp), g1 = min(NG, g0 + per_warp);
   uint4* out_masks = CR > 1 ? cl.map_shared_rank(gmasks, 0) : gmasks;
   const double lim = P.conf_logit;
+  const bool lim_zero = lim == 0.0;
   int count = 0;
   constexpr int U = 4;
   {
@@ -344,10 +345,21 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         if (g + k >= g1) break;
-        const unsigned m0 = __ballot_sync(FULL, (static_cast<double>(fgv[k].x) - static_cast<double>(bgv[k].x)) >= lim);
-        const unsigned m1 = __ballot_sync(FULL, (static_cast<double>(fgv[k].y) - static_cast<double>(bgv[k].y)) >= lim);
-        const unsigned m2 = __ballot_sync(FULL, (static_cast<double>(fgv[k].z) - static_cast<double>(bgv[k].z)) >= lim);
-        const unsigned m3 = __ballot_sync(FULL, (static_cast<double>(fgv[k].w) - static_cast<double>(bgv[k].w)) >= lim);
+        unsigned m0, m1, m2, m3;
+        if (lim_zero) {
+          // logit(0.5) = 0: the sign of an fp32 difference is the sign of
+          // the exact one (gradual underflow; inf - inf is NaN either way),
+          // so this equals the fp64 test without the fp32 -> fp64 conversions
+          m0 = __ballot_sync(FULL, fgv[k].x - bgv[k].x >= 0.0f);
+          m1 = __ballot_sync(FULL, fgv[k].y - bgv[k].y >= 0.0f);
+          m2 = __ballot_sync(FULL, fgv[k].z - bgv[k].z >= 0.0f);
+          m3 = __ballot_sync(FULL, fgv[k].w - bgv[k].w >= 0.0f);
+        } else {
+          m0 = __ballot_sync(FULL, (static_cast<double>(fgv[k].x) - static_cast<double>(bgv[k].x)) >= lim);
+          m1 = __ballot_sync(FULL, (static_cast<double>(fgv[k].y) - static_cast<double>(bgv[k].y)) >= lim);
+          m2 = __ballot_sync(FULL, (static_cast<double>(fgv[k].z) - static_cast<double>(bgv[k].z)) >= lim);
+          m3 = __ballot_sync(FULL, (static_cast<double>(fgv[k].w) - static_cast<double>(bgv[k].w)) >= lim);
+        }
         if (lane == 0) out_masks[g + k] = make_uint4(m0, m1, m2, m3);
         count += __popc(m0) + __popc(m1) + __popc(m2) + __popc(m3);
       }
@@ -914,6 +926,23 @@ __device__ __forceinline__ double cost_rounds(const CostView v, int worker, int 
           b[j][q] = y[lane + 32 * q];
         }
       }
+#ifdef TF_EXPERIMENT_NOCVT
+      // timing experiment only (wrong numerics): fp32 accumulation, no fp32 -> fp64 conversions
+      float accf[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) accf[j] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          accf[j] = fmaf(a[j][q].x, b[j][q].x, accf[j]);
+          accf[j] = fmaf(a[j][q].y, b[j][q].y, accf[j]);
+          accf[j] = fmaf(a[j][q].z, b[j][q].z, accf[j]);
+          accf[j] = fmaf(a[j][q].w, b[j][q].w, accf[j]);
+        }
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] = accf[j];
+#else
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -923,6 +952,7 @@ __device__ __forceinline__ double cost_rounds(const CostView v, int worker, int 
           acc[j] = fma(static_cast<double>(a[j][q].z), static_cast<double>(b[j][q].z), acc[j]);
           acc[j] = fma(static_cast<double>(a[j][q].w), static_cast<double>(b[j][q].w), acc[j]);
         }
+#endif
     } else {
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
