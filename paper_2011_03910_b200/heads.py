@@ -166,6 +166,9 @@ class BatchTracker:
 
     def _frames(self, n_streams: int, B: int, frame_index) -> np.ndarray:
         if frame_index is None:
+            if n_streams == 1:                     # (the host cost matters at small batches)
+                start = int(self.frame[0]) + 1
+                return np.arange(start, start + B, dtype=np.int64)
             return (self.frame[:n_streams, None] + 1 + np.arange(B)[None, :]).astype(np.int64).reshape(-1)
         return np.ascontiguousarray(frame_index, dtype=np.int64).reshape(-1)
 
@@ -208,7 +211,10 @@ class BatchTracker:
         if host:
             return OnlineTracks(host_out["count"], host_out["track_id"], host_out["box"], host_out["objectness"],
                                 frames, B)
-        return OnlineTracks(eng.rec_count[:F], eng.rec_id[:F], eng.rec_box[:F], eng.rec_obj[:F], frames, B)
+        views = self._views.get(F)
+        if views is None:
+            views = self._views[F] = (eng.rec_count[:F], eng.rec_id[:F], eng.rec_box[:F], eng.rec_obj[:F])
+        return OnlineTracks(*views, frames, B)
 
     def update_rows(self, rows, frame_index=None, *, stream_begin: int = 0, n_streams: int | None = None,
                     trace: bool = False, sync: bool = True) -> OnlineTracks:
@@ -276,15 +282,15 @@ class BatchTracker:
         later updates with the same shapes / strides / dtype only swap the data
         pointers (the per-update host cost matters at small batches)."""
         key = (host,) + tuple((t.shape, t.stride(), t.dtype, t.device) for t in (*out.heads, *out.embs))
-        if self._desc_key != key:
+        if self._desc_key != key:           # (a changed layout, dtype or device: validate and rebuild)
             self._desc = heads_descriptor(out, host, self.config.embedding_dim)
             self._desc_key = key
+            self._desc_scales = [self._desc.scale[i] for i in range(3)]   # views into the struct
             return self._desc
-        d = self._desc
-        for i in range(3):
-            d.scale[i].head = out.heads[i].data_ptr()
-            d.scale[i].emb = out.embs[i].data_ptr()
-        return d
+        for sc, h, e in zip(self._desc_scales, out.heads, out.embs):
+            sc.head = h.data_ptr()
+            sc.emb = e.data_ptr()
+        return self._desc
 
     def host_output(self, frames: int) -> dict:
         torch = self.engine.torch

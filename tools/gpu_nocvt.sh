@@ -7,3 +7,4 @@ timeout 600 python bench.py --no-cpu --no-cfg4 --config cfg4 > gpurun_out/nc_exp
 python -m paper_2011_03910_b200._build --force > /dev/null 2>&1
 timeout 600 python tools/b1_probe.py 1 300 > gpurun_out/b1_probe.txt 2>&1; echo b1=$?
 timeout 600 python tools/b1_probe.py 4 200 >> gpurun_out/b1_probe.txt 2>&1; echo b4=$?
+timeout 900 python -m pytest tests/test_gpu_heads.py tests/test_gpu_ties.py -q -x > gpurun_out/nc_tests.log 2>&1; echo tests=$?
