@@ -150,10 +150,17 @@ def require_cuda():
 
 
 def stream_handle(torch_stream=None) -> int:
+    """cudaStream_t of `torch_stream`, default torch's current stream on the
+    current device (read through the raw accessor: this runs per update and
+    its host cost shows at small batches)."""
     import torch
 
-    s = torch_stream or torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    if torch_stream is not None:
+        return int(torch_stream.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(torch._C._cuda_getDevice()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def ptr(t) -> int | None:

@@ -85,6 +85,8 @@ struct tf_ctx {
   long long prof_bytes_frame, prof_frames;
   long long* d_stats;
   int cluster_key, cluster_val;   // cached cluster size for the last stream count
+  int env_cluster = 0;            // TF_CLUSTER (read at tf_create)
+  bool env_zero_smem = false;     // TF_ZERO_SMEM (read at tf_create)
   std::vector<void*> allocs;
 };
 
@@ -239,6 +241,14 @@ cudaError_t upload_frame_index(tf_ctx* c, long long* dst, const long long* src, 
   return cudaEventRecord(c->ev_fidx[r], st);
 }
 
+// cudaSetDevice only when another device is current (per-update host cost)
+cudaError_t ensure_device(int device) {
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess || cur != device) e = cudaSetDevice(device);
+  return e;
+}
+
 cudaError_t prof_mark(tf_ctx* c, int which, cudaStream_t st) {
   if (!c->profiling || !c->prof_on) return cudaSuccess;
   const size_t idx = c->events_used + which;
@@ -293,6 +303,11 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   c->prof_frames = 0;
   c->cluster_key = -1;
   c->cluster_val = 1;
+  {
+    const char* ev = getenv("TF_CLUSTER");
+    c->env_cluster = ev ? atoi(ev) & 63 : 0;
+    c->env_zero_smem = getenv("TF_ZERO_SMEM") != nullptr;
+  }
   for (int b = 0; b < 2; ++b)
     for (int i = 0; i < 3; ++i) {
       c->stage_conf[b][i] = nullptr;
@@ -510,7 +525,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     if (rc) return rc;
   }
   c->prof_on = c->profiling && (c->prof_counter++ % c->prof_stride) == 0;
-  TF_CUDA(c, cudaSetDevice(c->device));
+  TF_CUDA(c, ensure_device(c->device));
   // buffer set and streams: without pipelining everything runs on `st` with set 0;
   // with pipelining the decode of this update (on `st`) overlaps the previous
   // update's association (on the side stream)
@@ -606,7 +621,9 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   // of this parity are read by the association two updates back, so only the
   // decode waits for it (the copy overlaps that association).
   if (c->pipeline && c->asc_pending[par]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[par], 0));
-  TF_CUDA(c, upload_frame_index(c, c->d_fidx[par], reinterpret_cast<const long long*>(frame_index), F, st));
+  const bool fidx_inline = F <= kFidxInline;      // small updates: indices travel in the launch parameters
+  if (!fidx_inline)
+    TF_CUDA(c, upload_frame_index(c, c->d_fidx[par], reinterpret_cast<const long long*>(frame_index), F, st));
   TF_CUDA(c, prof_mark(c, 0, st));
   TF_CUDA(c, launch_frame_heads(h, c->P, st));
   ++c->launches;
@@ -627,15 +644,19 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
   a.threads = c->assoc_threads;
-  a.zero_smem = getenv("TF_ZERO_SMEM") != nullptr;
+  a.zero_smem = c->env_zero_smem;
+  a.n_fidx_inline = 0;
+  if (fidx_inline) {
+    a.n_fidx_inline = F;
+    for (int i = 0; i < F; ++i) a.fidx_inline[i] = frame_index[i];
+  }
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
   a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
   {
-    const char* env = getenv("TF_CLUSTER");
-    const int key = n_streams * 64 + (env ? atoi(env) & 63 : 0);
+    const int key = n_streams * 64 + c->env_cluster;
     if (key != c->cluster_key) {
       c->cluster_val = a.threads == kAssocThreadsSmall ? 1 : assoc_cluster_size(n_streams, a.cap_tracks, a.cap_det, a.cap_entries);
       c->cluster_key = key;
@@ -716,7 +737,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   }
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   c->prof_on = c->profiling && (c->prof_counter++ % c->prof_stride) == 0;
-  TF_CUDA(c, cudaSetDevice(c->device));
+  TF_CUDA(c, ensure_device(c->device));
   for (int b = 0; b < 2; ++b)
     if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
   c->asc_pending[0] = c->asc_pending[1] = false;
@@ -736,15 +757,15 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
   a.threads = c->assoc_threads;
-  a.zero_smem = getenv("TF_ZERO_SMEM") != nullptr;
+  a.zero_smem = c->env_zero_smem;
+  a.n_fidx_inline = 0;
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
   a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
   {
-    const char* env = getenv("TF_CLUSTER");
-    const int key = n_streams * 64 + (env ? atoi(env) & 63 : 0);
+    const int key = n_streams * 64 + c->env_cluster;
     if (key != c->cluster_key) {
       c->cluster_val = a.threads == kAssocThreadsSmall ? 1 : assoc_cluster_size(n_streams, a.cap_tracks, a.cap_det, a.cap_entries);
       c->cluster_key = key;
@@ -784,10 +805,10 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   rc = check_ordering(c, stream, &fi, 1);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  TF_CUDA(c, cudaSetDevice(c->device));
+  TF_CUDA(c, ensure_device(c->device));
   for (int b = 0; b < 2; ++b)
     if (c->asc_pending[b]) TF_CUDA(c, cudaStreamWaitEvent(st, c->ev_asc[b], 0));
-  TF_CUDA(c, upload_frame_index(c, c->d_frame_index, &fi, 1, st));
+  // (the frame index travels in the association's launch parameters)
   TF_CUDA(c, launch_frame_dets(boxes, objectness, embeddings, has_embedding, n, c->cap.max_candidates,
                                c->cap.max_detections, c->det, c->P, st));
   ++c->launches;
@@ -802,7 +823,9 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.cap_det = c->cap.max_detections;
   a.cap_entries = c->cap_entries;
   a.threads = c->assoc_threads;
-  a.zero_smem = getenv("TF_ZERO_SMEM") != nullptr;
+  a.zero_smem = c->env_zero_smem;
+  a.n_fidx_inline = 1;
+  a.fidx_inline[0] = fi;
   a.pool_col = c->pool_col;
   a.pool_row = c->pool_row;
   a.pool_val = c->pool_val;

@@ -999,89 +999,6 @@ __device__ __noinline__ void cost_work(const CostView v, int worker, int n_worke
   }
 }
 
-// Single-CTA streams (many streams per GPU): the frame's entries grouped by
-// detection. A warp takes a detection column, loads and converts its row once
-// (16 fp64 per lane held in registers) and streams the column's track rows NB
-// at a time: the column's ~8 entries share one row load and one set of
-// fp32 -> fp64 conversions instead of one each (the cost phase of a lone CTA
-// is bound by L2 -> SM bytes and the conversion pipe). The per-entry
-// arithmetic -- products, lane order, shuffle tree -- is cost_rounds', so the
-// values are bit-identical to the cluster path's.
-template <int NB>
-__device__ __forceinline__ double cost_col_rounds(const CostView v, const int* cstart, const int16_t* cel, int K,
-                                                  int worker, int n_workers) {
-  const int lane = lane_id();
-  double amp = 0.0;
-  for (int k = worker; k < K; k += n_workers) {
-    const int e_beg = cstart[k], e_end = cstart[k + 1];
-    if (e_beg == e_end) continue;
-    double bd[16];
-    {
-      const float4* y = reinterpret_cast<const float4*>(v.dets + static_cast<long long>(k) * 512);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 t = y[lane + 32 * q];
-        bd[4 * q + 0] = static_cast<double>(t.x);
-        bd[4 * q + 1] = static_cast<double>(t.y);
-        bd[4 * q + 2] = static_cast<double>(t.z);
-        bd[4 * q + 3] = static_cast<double>(t.w);
-      }
-    }
-    for (int e0 = e_beg; e0 < e_end; e0 += NB) {
-      const int n = min(NB, e_end - e0);
-      int eid = 0, slot = 0;
-      if (lane < NB) {
-        eid = cel[e0 + min(lane, n - 1)];
-        slot = v.t_slot[v.erow[eid]];
-      }
-      int ej[NB], sl[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        ej[j] = __shfl_sync(FULL, eid, j);
-        sl[j] = __shfl_sync(FULL, slot, j);
-      }
-      float4 a[NB][4];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const float4* x = reinterpret_cast<const float4*>(v.pool + static_cast<long long>(sl[j]) * 512);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) a[j][q] = x[lane + 32 * q];
-      }
-      double acc[NB];
-#pragma unroll
-      for (int j = 0; j < NB; ++j) acc[j] = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          acc[j] = fma(static_cast<double>(a[j][q].x), bd[4 * q + 0], acc[j]);
-          acc[j] = fma(static_cast<double>(a[j][q].y), bd[4 * q + 1], acc[j]);
-          acc[j] = fma(static_cast<double>(a[j][q].z), bd[4 * q + 2], acc[j]);
-          acc[j] = fma(static_cast<double>(a[j][q].w), bd[4 * q + 3], acc[j]);
-        }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int j = 0; j < NB; ++j) acc[j] += __shfl_xor_sync(FULL, acc[j], o);
-#pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        if (j < n) {
-          const double c = fmin(fmax(1.0 - acc[j], 0.0), 2.0);
-          if (lane == 0) v.eval[ej[j]] = c;
-          amp = fmax(amp, c);
-        }
-      }
-    }
-  }
-  return amp;
-}
-
-__device__ __noinline__ void cost_work_cols(const CostView v, const int* cstart, const int16_t* cel, int K, int worker,
-                                            int n_workers) {
-  const double amp = cost_col_rounds<4>(v, cstart, cel, K, worker, n_workers);
-  if (lane_id() == 0) v.ampw[worker] = amp;
-}
-
 struct EmaView {
   const int* slot;             // pool slot of each detection's matched track, -1 if none
   int* work;
@@ -1462,7 +1379,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   __shared__ int s_fst[kFrameTable], s_fcnt[kFrameTable];
   for (int i = tid; i < a.B && i < kFrameTable; i += blockDim.x) {
     const int fi = ls * a.B + i;
-    s_fidx[i] = a.frame_index[fi];
+    s_fidx[i] = fi < a.n_fidx_inline ? a.fidx_inline[fi] : a.frame_index[fi];
     s_fst[i] = a.det.status[fi];
     s_fcnt[i] = min(a.det.count[fi], Km);
   }
@@ -1494,7 +1411,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     if (s_status != 0) break;                      // stream failed earlier: stop
     const int f = ls * a.B + b;
     const long long fK = static_cast<long long>(f) * Km;
-    const long long frame = b < kFrameTable ? s_fidx[b] : a.frame_index[f];
+    const long long frame = b < kFrameTable ? s_fidx[b] : f < a.n_fidx_inline ? a.fidx_inline[f] : a.frame_index[f];
     const int fst = b < kFrameTable ? s_fst[b] : a.det.status[f];
     if (fst != 0) {                                // decode/NMS error of this frame
       if (tid == 0) s_status = (b << 8) | fst;
@@ -1702,42 +1619,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       cv.dets = a.det.emb + fK * static_cast<long long>(D);
       cv.E = s_Efr;
       cv.D = D;
-      if (C == 1 && !kExt && D == 512 && cv.E > 0 && cv.E <= 32767) {
-        // lone CTA: entries grouped by detection (counting sort into the
-        // LAP's scratch, free until the LAP; the gate factors it overlaps
-        // are dead on the reference path)
-        int* cstart = reinterpret_cast<int*>(L.u);      // K + 1 column starts
-        int* cnext = reinterpret_cast<int*>(L.v);       // scatter cursors
-        const int E = cv.E;
-        for (int k = tid; k <= K; k += blockDim.x) cstart[k] = 0;
-        __syncthreads();
-        for (int e = tid; e < E; e += blockDim.x) atomicAdd(&cstart[ecol[e] + 1], 1);
-        __syncthreads();
-        if (wid == 0) {
-          int carry = 0;
-          for (int k0 = 0; k0 <= K; k0 += 32) {
-            const int k = k0 + lane;
-            const int v0 = k <= K ? cstart[k] : 0;
-            int incl = v0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int q = __shfl_up_sync(FULL, incl, o);
-              if (lane >= o) incl += q;
-            }
-            if (k <= K) {
-              cstart[k] = carry + incl;
-              cnext[k] = carry + incl;
-            }
-            carry += __shfl_sync(FULL, incl, 31);
-          }
-        }
-        __syncthreads();
-        for (int e = tid; e < E; e += blockDim.x) c_epos[atomicAdd(&cnext[ecol[e]], 1)] = static_cast<int16_t>(e);
-        __syncthreads();
-        cost_work_cols(cv, cstart, c_epos, K, wid, nw);
-      } else {
-        cost_work(cv, wid, nw * C);
-      }
+      cost_work(cv, wid, nw * C);
     }
     __syncthreads();
     TF_SUB(22);

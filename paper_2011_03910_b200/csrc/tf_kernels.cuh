@@ -7,6 +7,7 @@ namespace tfd {
 
 constexpr int kAssocThreads = 256;
 constexpr int kAssocThreadsSmall = 128;   // two association CTAs per SM (many streams)
+constexpr int kFidxInline = 32;           // frame indices passed in the launch parameters
 
 // Per-frame detection buffer written by the frame stage, read by associate_kernel.
 // Arrays are [frames][cap_det] (meas: x4, emb: xD).
@@ -61,7 +62,9 @@ struct AssocArgs {
   TrackBuf trk;
   OutBuf out;
   TraceBuf trace;
-  const long long* frame_index;  // [F] device
+  const long long* frame_index;  // [F] device (frames >= n_fidx_inline)
+  int n_fidx_inline;             // small updates pass their frame indices by value ...
+  long long fidx_inline[kFidxInline];   // ... (no per-update host->device copy)
   int stream_begin, B;
   int cap_tracks, cap_det, cap_entries;
   int16_t* pool_col;             // [streams][cap_tracks * cap_det] overflow CSR

@@ -1,0 +1,7 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_heads.py tests/test_gpu_ties.py tests/test_gpu_tracker.py tests/test_gpu_units.py -q -x > gpurun_out/r02g_tests.log 2>&1; echo tests=$?
+for c in "cfg4" "cfg1" "cfg1 --batch 1"; do
+  n=$(echo $c | tr -d ' -')
+  timeout 600 python bench.py --no-cpu --no-cfg4 --config $c > gpurun_out/r02g_$n.json 2> gpurun_out/r02g_$n.err; echo $n=$?
+done
+timeout 300 python tools/host_probe.py 1 > gpurun_out/r02g_host_b1.txt 2>&1
