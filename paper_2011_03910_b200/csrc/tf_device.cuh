@@ -270,7 +270,42 @@ __device__ inline int block_nms(int C, const double* box, const double* score, c
     }
   }
   __syncthreads();
-  if (wid == 0) {
+  if (wid == 0 && na <= 64) {
+    // Greedy order resolved in parallel (up to 64 boxes, two per lane): box u
+    // is kept iff no KEPT box before it suppresses it. Undecided boxes whose
+    // suppressors are all decided settle each pass, so the passes follow the
+    // longest suppression chain (1-3 in practice) instead of na serial steps.
+    unsigned long long in[2] = {0ull, 0ull};         // suppressors of boxes lane, lane + 32
+    for (int v = 0; v < na; ++v) {
+      const unsigned long long row = mask[v * words];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = lane + 32 * h;
+        if (v < u && ((row >> u) & 1ull)) in[h] |= 1ull << v;
+      }
+    }
+    const unsigned long long all = na == 64 ? ~0ull : (1ull << na) - 1ull;
+    unsigned long long kept = 0ull, supp = 0ull;
+    while ((kept | supp) != all) {
+      bool k[2], q[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = lane + 32 * h;
+        const bool open = u < na && !(((kept | supp) >> u) & 1ull);
+        q[h] = open && (in[h] & kept) != 0ull;
+        k[h] = open && !q[h] && (in[h] & ~supp) == 0ull;
+      }
+      kept |= static_cast<unsigned long long>(__ballot_sync(FULL, k[0])) |
+              (static_cast<unsigned long long>(__ballot_sync(FULL, k[1])) << 32);
+      supp |= static_cast<unsigned long long>(__ballot_sync(FULL, q[0])) |
+              (static_cast<unsigned long long>(__ballot_sync(FULL, q[1])) << 32);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int u = lane + 32 * h;
+      if (u < na && ((kept >> u) & 1ull)) keep[sorted[u]] = 1;
+    }
+  } else if (wid == 0) {
     unsigned long long removed = 0ull;   // lane l holds word l
     for (int u = 0; u < na; ++u) {
       unsigned long long word = __shfl_sync(FULL, removed, u >> 6);

@@ -162,6 +162,38 @@ __device__ int gather_normalize(const T* src, long long stride, int dim, int qua
                    (out == nullptr || (reinterpret_cast<uintptr_t>(out) & 15) == 0);
   double ss = 0.0;
   bool finite = true;
+  if (vec && dim == 512 && !quantize) {
+    // the common row: 16 values per lane held in registers, one read
+    float4 q[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) q[j] = Elt<T>::ld4(src + 4 * (lane + 32 * j));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      finite = finite && isfinite(q[j].x) && isfinite(q[j].y) && isfinite(q[j].z) && isfinite(q[j].w);
+      ss = fma(static_cast<double>(q[j].x), static_cast<double>(q[j].x), ss);
+      ss = fma(static_cast<double>(q[j].y), static_cast<double>(q[j].y), ss);
+      ss = fma(static_cast<double>(q[j].z), static_cast<double>(q[j].z), ss);
+      ss = fma(static_cast<double>(q[j].w), static_cast<double>(q[j].w), ss);
+    }
+    ss = warp_sum(ss);
+    finite = __all_sync(FULL, finite);
+    if (!finite) return TF_DEGENERATE_EMBEDDING;
+    const double norm = sqrt(ss);
+    if (norm < 1e-12) return TF_DEGENERATE_EMBEDDING;
+    if (out == nullptr) return TF_OK;
+    float4* o4 = reinterpret_cast<float4*>(out);
+    const double rn = __drcp_rn(norm);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float4 r;
+      r.x = static_cast<float>(div_by(static_cast<double>(q[j].x), norm, rn));
+      r.y = static_cast<float>(div_by(static_cast<double>(q[j].y), norm, rn));
+      r.z = static_cast<float>(div_by(static_cast<double>(q[j].z), norm, rn));
+      r.w = static_cast<float>(div_by(static_cast<double>(q[j].w), norm, rn));
+      o4[lane + 32 * j] = r;
+    }
+    return TF_OK;
+  }
   if (vec) {
     for (int i = lane; i < dim / 4; i += 32) {
       float4 q = Elt<T>::ld4(src + 4 * i);
@@ -234,6 +266,12 @@ __device__ int gather_normalize(const T* src, long long stride, int dim, int qua
 #ifndef TF_FRAME_MINB
 #define TF_FRAME_MINB 4   // 256-thread CTAs: <= 64 registers, 4 CTAs per SM (cfg4: 5 -> 0.58 ms with spills, 1 -> 90 registers, 0.88 ms)
 #endif
+#ifdef TF_FRAME_TIMERS
+// diagnostics: clock64 at the phase boundaries of frame 0's leader CTA, printed per launch
+#define TF_FT(i) if (f == 0 && crank == 0 && threadIdx.x == 0) ft[i] = clock64();
+#else
+#define TF_FT(i)
+#endif
 template <typename T, int kThreads>
 __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1) frame_heads_kernel(FrameArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -246,6 +284,10 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
   const int crank = static_cast<int>(cl.block_rank());
   const int f = blockIdx.x / CR;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
+#ifdef TF_FRAME_TIMERS
+  long long ft[10] = {0};
+#endif
+  TF_FT(0);
 
   __shared__ const T* s_bg[12];
   __shared__ const T* s_fg[12];
@@ -297,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
   uint8_t* ckeep = smem + plan.off_keep;
   int16_t* cpos = reinterpret_cast<int16_t*>(smem + plan.off_pos);
 
+  TF_FT(1);
   // ---- pass 1: confidence scan ---------------------------------------------
   // The 12 (scale, anchor) background / foreground plane pairs are split into
   // groups of 128 anchors; a lane owns 4 consecutive anchors (one float4 of
@@ -365,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
       }
     }
   }
+  TF_FT(2);
   // pass-2 ranges are the leader's own warps' over all groups
   int p0 = g0, p1 = g1;
   if (CR > 1) {
@@ -397,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
   const int C = min(C_all, a.cap_cand);
   if (tid == 0 && C_all > a.cap_cand) flag_error(&s_misc[0], 0, TF_CAPACITY);
 
+  TF_FT(3);
   // ---- pass 2: ordered compaction of candidate codes (anchor order) --------
   {
     int base = s_warp[wid];
@@ -418,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
   }
   __syncthreads();
 
+  TF_FT(4);
   // ---- candidate decode (sigmoid/exp boxes, letterbox inverse) -------------
   for (int r = tid; r < C; r += blockDim.x) {
     int g = ccode[r];
@@ -456,8 +502,10 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
   }
   __syncthreads();
 
+  TF_FT(5);
   // ---- NMS ------------------------------------------------------------------
   block_nms(C, cbox, cscore, calive, P.nms_iou, csorted, nmask, a.words, ckeep, &s_misc[1]);
+  TF_FT(6);
   const int K_all = block_rank(C, [&](int i) { return ckeep[i] != 0; }, cpos, s_warp);
   const int K = min(K_all, a.cap_det);
   if (tid == 0 && K_all > a.cap_det) flag_error(&s_misc[0], 0, TF_CAPACITY);
@@ -491,7 +539,15 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
     int st = gather_normalize(src, sc.es_c, D, P.quantize, out);
     if (st != TF_OK && lane == 0) flag_error(&s_misc[0], r + 1, st);
   }
+  TF_FT(7);
   __syncthreads();
+  TF_FT(8);
+#ifdef TF_FRAME_TIMERS
+  if (f == 0 && crank == 0 && tid == 0)
+    printf("TFFT C=%d K=%d setup %lld scan %lld sync %lld rank %lld decode %lld nms %lld gather %lld tail %lld\n", C, K,
+           ft[1] - ft[0], ft[2] - ft[1], ft[3] - ft[2], ft[4] - ft[3], ft[5] - ft[4], ft[6] - ft[5], ft[7] - ft[6],
+           ft[8] - ft[7]);
+#endif
   if (tid == 0) {
     a.det.count[f] = K;
     a.det.cand_count[f] = C_all;
@@ -1286,6 +1342,12 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     }
     cg::this_cluster().sync();
   }
+  // Programmatic dependent launch: the next association launch on this
+  // stream may be scheduled now and run its set-up (above) while this one
+  // works; it waits here for this grid's completion (and its memory) before
+  // touching the track tables and embedding pool that this launch writes.
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
   if (rank != 0) {
     // ---- follower CTA: joins the cost and EMA phases of every frame -------
@@ -3060,13 +3122,31 @@ static cudaError_t launch_associate_t(const AssocArgs& a, int n_streams, const P
 #endif
   if (a.threads == kAssocThreadsSmall) {
     set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreadsSmall, kExt>), smem);
-    associate_kernel<kAssocThreadsSmall, kExt><<<n_streams, kAssocThreadsSmall, smem, st>>>(a, P);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(n_streams));
+    cfg.blockDim = dim3(kAssocThreadsSmall);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, associate_kernel<kAssocThreadsSmall, kExt>, a, P);
   }
   set_smem(reinterpret_cast<const void*>(associate_kernel<kAssocThreads, kExt>), smem);
   if (a.cluster <= 1) {
-    associate_kernel<kAssocThreads, kExt><<<n_streams, kAssocThreads, smem, st>>>(a, P);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(n_streams));
+    cfg.blockDim = dim3(kAssocThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see griddepcontrol in the kernel
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, associate_kernel<kAssocThreads, kExt>, a, P);
   }
   if (kExt && a.cluster > 8) {          // (the reference-path instantiation is set up by assoc_cluster_size)
     static bool nonportable = false;
@@ -3079,13 +3159,15 @@ static cudaError_t launch_associate_t(const AssocArgs& a, int n_streams, const P
   cfg.blockDim = dim3(kAssocThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(a.cluster);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, associate_kernel<kAssocThreads, kExt>, a, P);
 }
 
