@@ -388,9 +388,11 @@ def streamed_updates(bt, gen_batch, K, F, stream, trace_counts):
     return ms
 
 
-def cfg4_block(args, world, rank, dev, barrier):
+def cfg4_block(args, world, rank, dev, barrier, shard_world=None):
     """Config 4 strong scaling at this N: 512 streams sharded over the ranks,
-    B = 8, batches generated between steps and each step timed alone."""
+    B = 8, batches generated between steps and each step timed alone.
+    ``shard_world`` > world runs rank 0's shard of a larger job on this GPU
+    (the per-GPU work at that many GPUs, e.g. 64 streams for 8)."""
     import torch
 
     import paper_2011_03910_b200 as p
@@ -398,7 +400,7 @@ def cfg4_block(args, world, rank, dev, barrier):
     from paper_2011_03910_b200.dist import gather_metrics, shard_streams, summarize
 
     cfg = synth.CONFIGS["cfg4"]
-    sh = shard_streams(cfg.streams, world, rank)
+    sh = shard_streams(cfg.streams, shard_world or world, rank)
     S, B = sh.n_streams, cfg.batch
     F = S * B
     gen = synth.make("cfg4", device=dev, seed=args.seed + 7 + rank, streams=S)
@@ -626,6 +628,17 @@ def run_ours(args):
         del batches
         torch.cuda.empty_cache()
         c4 = cfg4_block(args, world, rank, dev, barrier)
+        if world == 1 and args.cfg4_project:
+            # the per-GPU share at 2/4/8 GPUs, measured on this one: rank 0's
+            # shard of the 512 streams (no other rank exists; no collective)
+            proj = {}
+            for n in args.cfg4_project:
+                b = cfg4_block(args, 1, 0, dev, barrier, shard_world=n)
+                proj[str(n)] = {"streams_per_gpu": b["streams_per_rank"], "per_gpu_frames_per_s": b["frames_per_s"],
+                                "ms_per_step": b["ms_per_step"],
+                                "projected_total_frames_per_s": b["frames_per_s"] * n,
+                                "projected_scaling_vs_1": b["frames_per_s"] * n / c4["frames_per_s"]}
+            c4["per_gpu_share_at_n_gpus"] = proj
 
     if rank == 0:
         summ = summarize(per_rank)
@@ -738,6 +751,8 @@ def main():
     ap.add_argument("--cfg4-steps", type=int, default=4)
     ap.add_argument("--cfg4-warmup", type=int, default=3)
     ap.add_argument("--no-cfg4", action="store_true", help="skip the config-4 strong-scaling block")
+    ap.add_argument("--cfg4-project", type=int, nargs="*", default=[8],
+                    help="N=1 only: also time rank 0's cfg4 shard at these GPU counts (per-GPU work at N GPUs)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="serialise decode and association")
     ap.add_argument("--jde", action="store_true",
