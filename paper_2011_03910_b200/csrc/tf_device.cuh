@@ -802,8 +802,43 @@ __device__ inline void lap_row_arcs(int i, int nc, const Rows R, double sentinel
   }
 }
 
+// Fast pre-check for the common case of the transposed component (rows =
+// detections, their entries contiguous in R's list): one lane per ENTRY
+// instead of one lane per row walking its entries, so the dependent shared
+// loads of a row's entries overlap. Returns true when no row is active (the
+// optimum is unique; the usual outcome), false when lap_unique must build the
+// graph. Other row accessors are not pre-checked.
+template <class Rows>
+__device__ __forceinline__ bool lap_no_active_rows(int, int, const Rows&, double, double, const LapScratch&) {
+  return false;
+}
+__device__ __forceinline__ bool lap_no_active_rows(int nr, int nc, const TransposedRows& R, double sentinel,
+                                                   double eps, const LapScratch& s) {
+  const int lane = lane_id();
+  const int n_ent = R.begin(nr);
+  bool active = false;
+  for (int q = lane; q < n_ent; q += 32) {
+    int i = 0;
+    while (q >= R.begin(i + 1)) ++i;
+    const int j = R.col(q);
+    if (j < 0 || j >= nc || j == s.col4row[i]) continue;
+    if (R.val(q) - s.u[i] - s.v[j] <= eps) active = true;
+  }
+  for (int i = lane; i < nr; i += 32) {
+    const double ui = s.u[i];
+    if (ui >= sentinel - eps) {                       // a row with possible near-tight sentinel cells
+      const int ci = s.col4row[i];
+      const double theta = sentinel - ui - eps;
+      for (int j = 0; j < nc; ++j)
+        if (j != ci && s.v[j] >= theta) active = true;
+    }
+  }
+  return !__any_sync(FULL, active);
+}
+
 template <class Rows>
 __device__ inline bool lap_unique(int nr, int nc, const Rows R, double sentinel, double eps, LapScratch s) {
+  if (lap_no_active_rows(nr, nc, R, sentinel, eps, s)) return true;
   const int lane = lane_id();
   for (int j = lane; j < nc; j += 32) s.row4col[j] = -1;
   __syncwarp();

@@ -2106,9 +2106,14 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
             __syncwarp();
             warp_lap_fast(n_l, nc_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, Ls, nc_l);
             __syncwarp();
+#ifdef TF_EXPERIMENT_COUNT_LAPU
+            if (a.stats && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ph[14]), 1ull);
+#endif
+#ifndef TF_EXPERIMENT_NO_LAPU
             if (!lap_unique(nc_l, n_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, tie_eps, Ls) &&
                 lane == 0)
               s_alt = 1;
+#endif
             for (int j = lane; j < nc_l; j += 32) {
               const int lc = Ls.col4row[j];
               if (lc < nr_l) {
@@ -2120,9 +2125,14 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
           } else {
             warp_lap_fast(n_l, nr_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, Ls, nr_l);
             __syncwarp();
+#ifdef TF_EXPERIMENT_COUNT_LAPU
+            if (a.stats && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ph[10]), 1ull);
+#endif
+#ifndef TF_EXPERIMENT_NO_LAPU
             if (!lap_unique(nr_l, n_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, tie_eps,
                             Ls) && lane == 0)
               s_alt = 1;
+#endif
             for (int r = lane; r < nr_l; r += 32) {
               const int j = Ls.col4row[r];
               if (j < nc_l) {
