@@ -169,7 +169,7 @@ class BatchTracker:
             if n_streams == 1:                     # (the host cost matters at small batches)
                 start = int(self.frame[0]) + 1
                 return np.arange(start, start + B, dtype=np.int64)
-            return (self.frame[:n_streams, None] + 1 + np.arange(B)[None, :]).astype(np.int64).reshape(-1)
+            return np.add.outer(self.frame[:n_streams] + 1, np.arange(B, dtype=np.int64)).reshape(-1)
         return np.ascontiguousarray(frame_index, dtype=np.int64).reshape(-1)
 
     def update(self, head_outputs: HeadOutputs, frame_index=None, *, stream_begin: int = 0,
