@@ -223,6 +223,15 @@ int tf_join(tf_ctx* ctx, void* cuda_stream);
 /* Copy one stream's tracks into caller HOST buffers (synchronising). */
 int tf_export_tracks(tf_ctx* ctx, int32_t stream, tf_track_export* out, void* cuda_stream);
 
+/* Inverse of tf_export_tracks (synchronising): make `in` (count tracks in
+ * Tracker.tracks order, next_id, last_frame) stream's state, e.g. a reference
+ * Tracker's tracks / _next_id / _last_frame at some frame (tf/tracker.py:74-83),
+ * so a sequence resumes from it (parity bisection). TF_ARGUMENT for ids outside
+ * [1, next_id) or repeated, a state other than 0/1, lost_since set for an
+ * ACTIVE track (or -1 for a LOST one), or a covariance outside the per-axis
+ * (position, velocity) form the filter keeps; TF_CAPACITY above max_tracks. */
+int tf_import_tracks(tf_ctx* ctx, int32_t stream, const tf_track_export* in, void* cuda_stream);
+
 /* Optional CUDA-event timing of the two kernels of every update (bench.py).
  * enabled: 0 off, 1 kernel events, 2 kernel events + the association
  * kernel's in-kernel phase timers (tf_phase_stats; they cost ~1% of the

@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *objs,
-           "-cudart", "static", "-Xcompiler", "-fPIC"]
+           "-cudart", "static", "-Xcompiler", "-fPIC", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")

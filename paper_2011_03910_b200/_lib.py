@@ -57,6 +57,9 @@ class TfTrace(C.Structure):
                 ("det_cost", c_vp), ("det_matched", c_vp)]
 
 
+NO_FRAME = -(2 ** 63)  # tf_track_export.last_frame before the first step (_last_frame None)
+
+
 class TfTrackExport(C.Structure):
     _fields_ = [("count", c_i32), ("reserved", c_i32), ("next_id", c_i64), ("last_frame", c_i64),
                 ("track_id", c_vp), ("state", c_vp), ("hits", c_vp), ("lost_since", c_vp),
@@ -77,6 +80,7 @@ _SIGS = {
                                    C.POINTER(TfRecords), C.POINTER(TfTrace), c_vp]),
     "tf_finish": (c_i32, [c_vp, c_vp]),
     "tf_export_tracks": (c_i32, [c_vp, c_i32, C.POINTER(TfTrackExport), c_vp]),
+    "tf_import_tracks": (c_i32, [c_vp, c_i32, C.POINTER(TfTrackExport), c_vp]),
     "tf_set_pipeline": (c_i32, [c_vp, c_i32]),
     "tf_join": (c_i32, [c_vp, c_vp]),
     "tf_set_profiling": (c_i32, [c_vp, c_i32]),

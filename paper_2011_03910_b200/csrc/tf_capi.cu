@@ -16,7 +16,31 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "tf_kernels.cuh"
+
+// NVTX ranges around the host entry points (SURVEY.md section 5 tracing: the
+// reference's per-stage timers). A no-op unless a tool (ncu, nsys) injects.
+namespace {
+nvtxDomainHandle_t nvtx_domain() {
+  static nvtxDomainHandle_t d = nvtxDomainCreateA("trackforge_b200");
+  return d;
+}
+struct NvtxRange {
+  explicit NvtxRange(const char* name) {
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    nvtxDomainRangePushEx(nvtx_domain(), &a);
+  }
+  ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 using namespace tfd;
 
@@ -267,7 +291,7 @@ cudaError_t prof_mark(tf_ctx* c, int which, cudaStream_t st) {
 
 extern "C" {
 
-int tf_version(void) { return 2; }   // 2: tf_head_scale.channels is checked
+int tf_version(void) { return 3; }   // 2: tf_head_scale.channels is checked; 3: tf_import_tracks
 
 const char* tf_status_name(int status) {
   if (status < 0 || status > TF_ARGUMENT) return "UnknownError";
@@ -465,6 +489,7 @@ int tf_destroy(tf_ctx* ctx) {
 }
 
 int tf_reset_stream(tf_ctx* c, int32_t stream, void* cuda_stream) {
+  NvtxRange nvtx_range("tf_reset_stream");
   if (!c) return TF_ARGUMENT;
   if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -498,6 +523,7 @@ static int ensure_record_staging(tf_ctx* c, int frames, int max_records) {
 int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int32_t n_streams,
                     int32_t B, const int64_t* frame_index, const tf_records* out, const tf_trace* trace,
                     void* cuda_stream) {
+  NvtxRange nvtx_range("tf_update_heads");
   if (!c || !heads || !frame_index || !out) return fail(c, TF_ARGUMENT, "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   if (n_streams < 1 || B < 1 || stream_begin < 0 || stream_begin + n_streams > c->cap.streams)
@@ -716,6 +742,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
                          const int32_t* row_offsets, const double* boxes, const double* objectness,
                          const float* embeddings, int32_t normalized, const tf_records* out, const tf_trace* trace,
                          void* cuda_stream) {
+  NvtxRange nvtx_range("tf_update_detections");
   if (!c || !frame_index || !row_offsets || !out) return fail(c, TF_ARGUMENT, "null argument");
   if (n_streams < 1 || B < 1 || stream_begin < 0 || stream_begin + n_streams > c->cap.streams)
     return fail(c, TF_ARGUMENT, "stream range out of bounds");
@@ -793,6 +820,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
 int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n, const double* boxes,
                        const double* objectness, const float* embeddings, const uint8_t* has_embedding,
                        const tf_records* out, const tf_trace* trace, void* cuda_stream) {
+  NvtxRange nvtx_range("tf_step_detections");
   if (!c || !out) return fail(c, TF_ARGUMENT, "null argument");
   if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
   if (n < 0) return fail(c, TF_ARGUMENT, "negative detection count");
@@ -850,6 +878,7 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
 }
 
 int tf_finish(tf_ctx* c, void* cuda_stream) {
+  NvtxRange nvtx_range("tf_finish");
   if (!c) return TF_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   TF_CUDA(c, cudaStreamSynchronize(st));
@@ -896,6 +925,7 @@ int tf_join(tf_ctx* c, void* cuda_stream) {
 }
 
 int tf_export_tracks(tf_ctx* c, int32_t stream, tf_track_export* o, void* cuda_stream) {
+  NvtxRange nvtx_range("tf_export_tracks");
   if (!c || !o) return TF_ARGUMENT;
   if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -934,6 +964,76 @@ int tf_export_tracks(tf_ctx* c, int32_t stream, tf_track_export* o, void* cuda_s
     TF_CUDA(c, cudaMemcpy(o->embedding + D * t, c->trk.emb_pool + (base + slot[t]) * D, 4 * D,
                           cudaMemcpyDeviceToHost));
   }
+  return TF_OK;
+}
+
+int tf_import_tracks(tf_ctx* c, int32_t stream, const tf_track_export* in, void* cuda_stream) {
+  NvtxRange nvtx_range("tf_import_tracks");
+  // inverse of tf_export_tracks: the track table of a Tracker at some frame
+  // (tf/tracker.py:74-83 tracks, _next_id, _last_frame) becomes stream's
+  // state, so a sequence can be resumed from the reference's state at any
+  // frame (parity bisection). Slots are re-packed 0..count-1.
+  if (!c || !in) return TF_ARGUMENT;
+  if (stream < 0 || stream >= c->cap.streams) return fail(c, TF_ARGUMENT, "stream out of range");
+  const int n = in->count;
+  const int Tm = c->cap.max_tracks, D = c->cfg.embedding_dim;
+  if (n < 0 || n > Tm)
+    return fail(c, TF_CAPACITY, "import of " + std::to_string(n) + " tracks exceeds max_tracks " +
+                                    std::to_string(Tm));
+  if (n > 0 && (!in->track_id || !in->state || !in->hits || !in->lost_since || !in->last_update_frame ||
+                !in->mean || !in->covariance || !in->embedding))
+    return fail(c, TF_ARGUMENT, "import: NULL track array");
+  std::vector<double> cov(12 * static_cast<size_t>(n));
+  std::vector<int> slot(n), free_stack(Tm);
+  for (int t = 0; t < n; ++t) {
+    const long long id = in->track_id[t];
+    if (id < 1 || id >= in->next_id)
+      return fail(c, TF_ARGUMENT, "import: track id " + std::to_string(id) + " outside [1, next_id)");
+    for (int u = 0; u < t; ++u)
+      if (in->track_id[u] == id) return fail(c, TF_ARGUMENT, "import: duplicate track id " + std::to_string(id));
+    if (in->state[t] != 0 && in->state[t] != 1)
+      return fail(c, TF_ARGUMENT, "import: track state must be 0 (ACTIVE) or 1 (LOST)");
+    if ((in->state[t] == 1) != (in->lost_since[t] >= 0))
+      return fail(c, TF_ARGUMENT, "import: lost_since must be set exactly for LOST tracks");
+    const double* C8 = in->covariance + 64 * static_cast<size_t>(t);
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j)
+        if ((i & 3) != (j & 3) && C8[8 * i + j] != 0.0)
+          return fail(c, TF_ARGUMENT, "import: covariance of track " + std::to_string(id) +
+                                          " couples two axes; the filter keeps per-axis (position, velocity) blocks");
+    for (int i = 0; i < 4; ++i) {
+      if (C8[8 * i + i + 4] != C8[8 * (i + 4) + i])
+        return fail(c, TF_ARGUMENT, "import: covariance of track " + std::to_string(id) + " is not symmetric");
+      cov[12 * t + 3 * i] = C8[8 * i + i];
+      cov[12 * t + 3 * i + 1] = C8[8 * i + i + 4];
+      cov[12 * t + 3 * i + 2] = C8[8 * (i + 4) + i + 4];
+    }
+    slot[t] = t;
+  }
+  for (int i = 0; i < Tm; ++i) free_stack[i] = Tm - 1 - i;  // pops slot n next, as after n births
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  TF_CUDA(c, cudaStreamSynchronize(st));
+  if (c->side) TF_CUDA(c, cudaStreamSynchronize(c->side));
+  const long long base = static_cast<long long>(stream) * Tm;
+  const int nfree = Tm - n, zero = 0;
+  if (n > 0) {
+    TF_CUDA(c, cudaMemcpy(c->trk.id + base, in->track_id, 8 * n, cudaMemcpyHostToDevice));
+    TF_CUDA(c, cudaMemcpy(c->trk.state + base, in->state, 4 * n, cudaMemcpyHostToDevice));
+    TF_CUDA(c, cudaMemcpy(c->trk.hits + base, in->hits, 4 * n, cudaMemcpyHostToDevice));
+    TF_CUDA(c, cudaMemcpy(c->trk.lost + base, in->lost_since, 8 * n, cudaMemcpyHostToDevice));
+    TF_CUDA(c, cudaMemcpy(c->trk.last + base, in->last_update_frame, 8 * n, cudaMemcpyHostToDevice));
+    TF_CUDA(c, cudaMemcpy(c->trk.mean + base * 8, in->mean, 64 * n, cudaMemcpyHostToDevice));
+    TF_CUDA(c, cudaMemcpy(c->trk.cov + base * 12, cov.data(), 96 * n, cudaMemcpyHostToDevice));
+    TF_CUDA(c, cudaMemcpy(c->trk.slot + base, slot.data(), 4 * n, cudaMemcpyHostToDevice));
+    TF_CUDA(c, cudaMemcpy(c->trk.emb_pool + base * D, in->embedding, 4ll * D * n, cudaMemcpyHostToDevice));
+  }
+  TF_CUDA(c, cudaMemcpy(c->trk.free_stack + base, free_stack.data(), 4ll * Tm, cudaMemcpyHostToDevice));
+  TF_CUDA(c, cudaMemcpy(c->trk.n_free + stream, &nfree, 4, cudaMemcpyHostToDevice));
+  TF_CUDA(c, cudaMemcpy(c->trk.n_tracks + stream, &n, 4, cudaMemcpyHostToDevice));
+  TF_CUDA(c, cudaMemcpy(c->trk.next_id + stream, &in->next_id, 8, cudaMemcpyHostToDevice));
+  TF_CUDA(c, cudaMemcpy(c->trk.last_frame + stream, &in->last_frame, 8, cudaMemcpyHostToDevice));
+  TF_CUDA(c, cudaMemcpy(c->trk.status + stream, &zero, 4, cudaMemcpyHostToDevice));
+  c->last_frame[stream] = in->last_frame;
   return TF_OK;
 }
 

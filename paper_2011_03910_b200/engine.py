@@ -124,3 +124,24 @@ class Engine:
         res = {k: v[:n] for k, v in out.items()}
         res["count"], res["next_id"], res["last_frame"] = n, ex.next_id, ex.last_frame
         return res
+
+    def import_(self, s: int, state: dict) -> None:
+        """Make ``state`` (the dict ``export`` returns) stream s's track table
+        (tf_import_tracks; synchronising)."""
+        import numpy as np
+
+        n = int(state["count"])
+        D = self.dim
+        arrs = dict(track_id=np.ascontiguousarray(state["track_id"][:n], np.int64),
+                    state=np.ascontiguousarray(state["state"][:n], np.int32),
+                    hits=np.ascontiguousarray(state["hits"][:n], np.int32),
+                    lost_since=np.ascontiguousarray(state["lost_since"][:n], np.int64),
+                    last_update_frame=np.ascontiguousarray(state["last_update_frame"][:n], np.int64),
+                    mean=np.ascontiguousarray(np.reshape(state["mean"][:n], (n, 8)), np.float64),
+                    covariance=np.ascontiguousarray(np.reshape(state["covariance"][:n], (n, 8, 8)), np.float64),
+                    embedding=np.ascontiguousarray(np.reshape(state["embedding"][:n], (n, D)), np.float32))
+        ex = _lib.TfTrackExport()
+        ex.count, ex.next_id, ex.last_frame = n, int(state["next_id"]), int(state["last_frame"])
+        for k, v in arrs.items():
+            setattr(ex, k, v.ctypes.data)
+        self.check(self.lib.tf_import_tracks(self.ctx, s, C.byref(ex), _lib.stream_handle()), "import")

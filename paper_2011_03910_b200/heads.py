@@ -164,12 +164,13 @@ class BatchTracker:
         """Synchronise and raise the first device-side error of the queued updates."""
         self.engine.finish()
 
-    def _frames(self, n_streams: int, B: int, frame_index) -> np.ndarray:
+    def _frames(self, stream_begin: int, n_streams: int, B: int, frame_index) -> np.ndarray:
         if frame_index is None:
             if n_streams == 1:                     # (the host cost matters at small batches)
-                start = int(self.frame[0]) + 1
+                start = int(self.frame[stream_begin]) + 1
                 return np.arange(start, start + B, dtype=np.int64)
-            return np.add.outer(self.frame[:n_streams] + 1, np.arange(B, dtype=np.int64)).reshape(-1)
+            last = self.frame[stream_begin:stream_begin + n_streams]
+            return np.add.outer(last + 1, np.arange(B, dtype=np.int64)).reshape(-1)
         return np.ascontiguousarray(frame_index, dtype=np.int64).reshape(-1)
 
     def update(self, head_outputs: HeadOutputs, frame_index=None, *, stream_begin: int = 0,
@@ -191,7 +192,7 @@ class BatchTracker:
             raise LayoutError("host inputs must be pinned (torch.Tensor.pin_memory())")
         if not host and head_outputs.heads[0].device != eng.device:
             raise LayoutError(f"head tensors are on {head_outputs.heads[0].device}, the tracker on {eng.device}")
-        frames = self._frames(n_streams, B, frame_index)
+        frames = self._frames(stream_begin, n_streams, B, frame_index)
         desc = self._descriptor(head_outputs, host)
         if host:
             if host_out is None:
@@ -261,7 +262,7 @@ class BatchTracker:
         db = torch.as_tensor(boxes).to(dev)
         do = torch.as_tensor(np.ascontiguousarray(allr[:, 4])).to(dev)
         de = torch.as_tensor(np.ascontiguousarray(emb32)).to(dev)
-        frames = self._frames(n_streams, B, frame_index)
+        frames = self._frames(stream_begin, n_streams, B, frame_index)
         code = eng.lib.tf_update_detections(eng.ctx, stream_begin, n_streams, B, frames.ctypes.data,
                                             offsets.ctypes.data, db.data_ptr() if allr.shape[0] else None,
                                             do.data_ptr() if allr.shape[0] else None,
@@ -308,3 +309,10 @@ class BatchTracker:
 
     def export(self, stream: int) -> dict:
         return self.engine.export(stream)
+
+    def import_tracks(self, stream: int, state: dict) -> None:
+        """Inverse of ``export``: resume ``stream`` from a track table
+        (tf_import_tracks). Waits for the stream's pending updates."""
+        self.engine.import_(stream, state)
+        lf = int(state["last_frame"])
+        self.frame[stream] = -1 if lf == _lib.NO_FRAME else lf

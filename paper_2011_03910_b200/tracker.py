@@ -168,6 +168,50 @@ class Tracker:
                 hits=int(ex["hits"][i])))
         return out
 
+    def load_state(self, tracks: list[Track], *, next_id: int, last_frame: int | None) -> None:
+        """Resume from a track table: the reference Tracker's ``tracks``,
+        ``_next_id`` and ``_last_frame`` at some frame (tf/tracker.py:74-83)
+        become this tracker's state (tf_import_tracks), so one frame can be
+        re-run on the GPU from the reference's exact state."""
+        n = len(tracks)
+        D = self.config.embedding_dim
+        state = dict(count=n, next_id=int(next_id),
+                     last_frame=_lib.NO_FRAME if last_frame is None else int(last_frame),
+                     track_id=np.array([t.track_id for t in tracks], np.int64),
+                     state=np.array([1 if t.state.value == TrackState.LOST.value else 0 for t in tracks],
+                                    np.int32),
+                     hits=np.array([t.hits for t in tracks], np.int32),
+                     lost_since=np.array([-1 if t.lost_since is None else t.lost_since for t in tracks],
+                                         np.int64),
+                     last_update_frame=np.array([t.last_update_frame for t in tracks], np.int64),
+                     mean=np.array([np.asarray(t.kalman.mean, np.float64) for t in tracks]).reshape(n, 8),
+                     covariance=np.array([np.asarray(t.kalman.covariance, np.float64) for t in tracks]
+                                         ).reshape(n, 8, 8),
+                     embedding=np.array([np.asarray(t.smooth_embedding, np.float32) for t in tracks]
+                                        ).reshape(n, D))
+        for t in tracks:
+            if t.state.value not in (TrackState.ACTIVE.value, TrackState.LOST.value):
+                raise ValueError(f"track {t.track_id}: only ACTIVE and LOST tracks are held, got {t.state}")
+            if np.shape(t.smooth_embedding) != (D,):
+                raise DimensionError(f"track {t.track_id}: embedding shape {np.shape(t.smooth_embedding)} "
+                                     f"does not match embedding_dim {D}")
+        self._engine.import_(0, state)
+        self._snapshot = None
+
+    @classmethod
+    def from_reference(cls, tracker, *, capacity: Capacity | None = None, quantize: bool = False) -> "Tracker":
+        """A GPU tracker holding a reference ``trackforge.Tracker``'s current
+        state (config, tracks, id counter, last frame)."""
+        cfg = tracker.config
+        kw = {f: getattr(cfg, f) for f in TrackerConfig.__dataclass_fields__ if hasattr(cfg, f)}
+        if "motion_noise" in kw:
+            mn = kw["motion_noise"]
+            kw["motion_noise"] = MotionNoise(**{f: getattr(mn, f) for f in MotionNoise.__dataclass_fields__})
+        mine = TrackerConfig(**kw)
+        out = cls(mine, capacity=capacity, quantize=quantize)
+        out.load_state(list(tracker.tracks), next_id=tracker._next_id, last_frame=tracker._last_frame)
+        return out
+
     @property
     def removed_ids(self) -> set[int]:
         """Ids issued and no longer live: ids are never reused (tf/tracker.py:80, 139-140)."""

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     for name in decl:
         assert hasattr(lib, name), name
     assert set(decl) == set(_lib.EXPORTED)
-    assert lib.tf_version() == 2
+    assert lib.tf_version() == 3
     assert lib.tf_status_name(7) == b"ConfigError"
     assert lib.tf_status_name(8) == b"OrderingError"
 
