@@ -263,6 +263,11 @@ int tf_timeline(tf_ctx* ctx, double* out, int32_t max_updates, int32_t* n_update
  * [16] components + tie check [17] peeling [18] residual components
  * [19] warp solves [20] full restatement (ties). out has 32 entries. */
 int tf_phase_stats(tf_ctx* ctx, int64_t* out32);
+/* Per-stream association clocks of the last update run with profiling bit 2
+ * (tf_set_profiling(ctx, 4 | ...); diagnostics, synchronising): out[4s..4s+3]
+ * = the leader CTA's %globaltimer (ns) at entry, after the prologue (state
+ * loaded), after the last frame, and at exit. n_streams <= the context's. */
+int tf_stream_clocks(tf_ctx* ctx, int64_t* out, int32_t n_streams);
 
 /* ---- stage-level entry points (batched; device pointers) ---------------- */
 

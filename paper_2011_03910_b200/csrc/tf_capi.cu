@@ -107,7 +107,21 @@ struct tf_ctx {
   size_t events_used;
   double last_h2d_ms;              // host->device copy time of the last tf_kernel_times window
   long long prof_bytes_frame, prof_frames;
-  long long* d_stats;
+  long long* d_stats;            // [32] phase stats, then [streams][4] leader clocks (profiling bit 2)
+  int n_streams_alloc = 0;
+  int sms = 0;                    // SM count of the device
+  // longest-first order of single-CTA streams over more than one wave (associate_kernel)
+  int* d_order = nullptr;
+  long long* d_work = nullptr;
+  unsigned* d_ticket = nullptr;
+  long long order_key = -1;       // (stream_begin, n_streams) the order in d_order was computed for
+  int assoc_slots = 0;            // association CTAs resident at once
+  bool env_no_lpt = false;        // TF_NO_LPT (read at tf_create): identity order
+  // overlapped decode + association within one update (frame_heads_kernel overlapped mode)
+  unsigned* d_ready = nullptr;    // [max_frames] per-frame decode flags (epoch values)
+  int* d_fticket = nullptr;       // [2] the persistent decode grid's counters
+  unsigned epoch = 0;
+  bool env_overlap = false;       // TF_OVERLAP (read at tf_create): opt-in, see tf_update_heads
   int cluster_key, cluster_val;   // cached cluster size for the last stream count
   int env_cluster = 0;            // TF_CLUSTER (read at tf_create)
   bool env_zero_smem = false;     // TF_ZERO_SMEM (read at tf_create)
@@ -289,6 +303,34 @@ cudaError_t prof_mark(tf_ctx* c, int which, cudaStream_t st) {
 
 }  // namespace
 
+// Longest-first stream order for single-CTA association launches that need
+// more than one wave of CTAs: the kernel's last CTA ranks the streams by their
+// measured work for the next launch over the same streams (lpt_order).
+static bool uses_stream_order(const tf_ctx* c, int cluster, int n_streams) {
+  return cluster <= 1 && n_streams > c->assoc_slots && !c->env_no_lpt;
+}
+static long long order_key(int stream_begin, int n_streams) {
+  return (static_cast<long long>(stream_begin) << 32) | static_cast<unsigned>(n_streams);
+}
+// the block order the next association over these streams will use (nullptr = identity)
+static const int* next_stream_order(const tf_ctx* c, int cluster, int stream_begin, int n_streams) {
+  return uses_stream_order(c, cluster, n_streams) && order_key(stream_begin, n_streams) == c->order_key ? c->d_order
+                                                                                                        : nullptr;
+}
+static void set_stream_order(tf_ctx* c, AssocArgs& a, int stream_begin, int n_streams) {
+  a.order_in = nullptr;
+  a.order_out = nullptr;
+  a.work = c->d_work;
+  a.ticket = c->d_ticket;
+  if (!uses_stream_order(c, a.cluster, n_streams)) {
+    c->order_key = -1;
+    return;
+  }
+  a.order_in = next_stream_order(c, a.cluster, stream_begin, n_streams);
+  a.order_out = c->d_order;
+  c->order_key = order_key(stream_begin, n_streams);
+}
+
 extern "C" {
 
 int tf_version(void) { return 3; }   // 2: tf_head_scale.channels is checked; 3: tf_import_tracks
@@ -426,7 +468,20 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   A(&c->pool_row, S * Tm * Km);
   A(&c->pool_val, S * Tm * Km);
   A(&c->pool_aux, 2 * S * Tm * Km);
-  A(&c->d_stats, 32);
+  A(&c->d_stats, 32 + 4 * S);
+  A(&c->d_order, S);
+  A(&c->d_work, S);
+  A(&c->d_ticket, 1);
+  if (e == cudaSuccess) e = cudaMemset(c->d_ticket, 0, sizeof(unsigned));
+  A(&c->d_ready, F);
+  A(&c->d_fticket, 2);
+  if (e == cudaSuccess) e = cudaMemset(c->d_ready, 0, sizeof(unsigned) * F);
+  if (e == cudaSuccess) e = cudaMemset(c->d_fticket, 0, sizeof(int) * 2);
+  c->env_overlap = getenv("TF_OVERLAP") != nullptr;
+  c->assoc_slots = sms * (c->assoc_threads == kAssocThreadsSmall ? 2 : 1);
+  c->sms = sms;
+  c->env_no_lpt = getenv("TF_NO_LPT") != nullptr;
+  c->n_streams_alloc = static_cast<int>(S);
   if (e != cudaSuccess) {
     std::string m = cudaGetErrorString(e);
     tf_destroy(c);
@@ -560,7 +615,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   cudaStream_t ast = c->pipeline ? c->side : st;           // association + outputs
   DetBuf& det = c->dets[par];
 
-  HeadLaunch h;
+  HeadLaunch h = {};
   h.heads = heads;
   h.frames = F;
   h.cap_cand = c->cap.max_candidates;
@@ -650,16 +705,38 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   const bool fidx_inline = F <= kFidxInline;      // small updates: indices travel in the launch parameters
   if (!fidx_inline)
     TF_CUDA(c, upload_frame_index(c, c->d_fidx[par], reinterpret_cast<const long long*>(frame_index), F, st));
+  // Overlapped mode (opt-in, TF_OVERLAP): many frames, no pipelining,
+  // device-resident heads and single-CTA 128-thread association CTAs (one
+  // fits next to two decode CTAs on an SM): the decode grid is persistent and
+  // publishes frames one by one; the association starts right away
+  // (programmatic dependent launch) and waits per frame. No event may sit
+  // between the two launches. Measured on B200 at config 4 it is slower
+  // (2.45 vs 2.20 ms per step: while the decode runs, only one association
+  // CTA per SM fits instead of two, and the association needs every slot),
+  // so it is off by default; DESIGN.md section 6.
+  const bool overlap = !c->pipeline && !heads->host_memory && c->env_overlap &&
+                       c->assoc_threads == kAssocThreadsSmall && F >= 2 * c->sms;
+  h.ready = nullptr;
+  if (overlap) {
+    h.ready = c->d_ready;
+    h.epoch = ++c->epoch == 0 ? ++c->epoch : c->epoch;
+    h.ticket = c->d_fticket;
+    h.order = next_stream_order(c, 1, stream_begin, n_streams);
+    h.first_wave = c->sms;
+    h.streams = n_streams;
+    h.B = B;
+    h.persist_ctas = 2 * c->sms;
+  }
   TF_CUDA(c, prof_mark(c, 0, st));
   TF_CUDA(c, launch_frame_heads(h, c->P, st));
   ++c->launches;
-  TF_CUDA(c, prof_mark(c, 1, st));
+  if (!overlap) TF_CUDA(c, prof_mark(c, 1, st));
   if (c->pipeline) {
     TF_CUDA(c, cudaEventRecord(c->ev_dec[par], st));
     TF_CUDA(c, cudaStreamWaitEvent(ast, c->ev_dec[par], 0));
   }
 
-  AssocArgs a;
+  AssocArgs a = {};
   a.det = det;
   a.trk = c->trk;
   a.trace = to_trace(trace);
@@ -681,6 +758,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
   a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
+  a.sclk = (c->profiling & 4) ? c->d_stats + 32 : nullptr;
   {
     const int key = n_streams * 64 + c->env_cluster;
     if (key != c->cluster_key) {
@@ -689,6 +767,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     }
     a.cluster = c->cluster_val;
   }
+  set_stream_order(c, a, stream_begin, n_streams);
   const bool host_out = heads->host_memory != 0;
   if (host_out) {
     rc = ensure_record_staging(c, F, out->max_records);
@@ -706,9 +785,15 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
     a.out.objectness = out->objectness;
   }
   a.out.max_records = out->max_records;
-  TF_CUDA(c, prof_mark(c, 2, ast));
+  a.ready = overlap ? c->d_ready : nullptr;
+  a.epoch = h.epoch;
+  if (!overlap) TF_CUDA(c, prof_mark(c, 2, ast));
   TF_CUDA(c, launch_associate(a, n_streams, c->P, ast));
   ++c->launches;
+  if (overlap) {           // decode and association overlap: the frame slot times both, the association slot ~0
+    TF_CUDA(c, prof_mark(c, 1, ast));
+    TF_CUDA(c, prof_mark(c, 2, ast));
+  }
   TF_CUDA(c, prof_mark(c, 3, ast));
   if (c->pipeline) {
     TF_CUDA(c, cudaEventRecord(c->ev_asc[par], ast));
@@ -773,7 +858,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   TF_CUDA(c, launch_frame_rows(boxes, objectness, embeddings, c->d_row_offsets, F, normalized ? 0 : 1,
                                c->cap.max_candidates, c->cap.max_detections, c->det, c->P, st));
   ++c->launches;
-  AssocArgs a;
+  AssocArgs a = {};
   a.det = c->det;
   a.trk = c->trk;
   a.trace = to_trace(trace);
@@ -791,6 +876,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
   a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
+  a.sclk = (c->profiling & 4) ? c->d_stats + 32 : nullptr;
   {
     const int key = n_streams * 64 + c->env_cluster;
     if (key != c->cluster_key) {
@@ -799,6 +885,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
     }
     a.cluster = c->cluster_val;
   }
+  set_stream_order(c, a, stream_begin, n_streams);
   a.out.count = out->count;
   a.out.track_id = reinterpret_cast<long long*>(out->track_id);
   a.out.box = out->box;
@@ -840,7 +927,7 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   TF_CUDA(c, launch_frame_dets(boxes, objectness, embeddings, has_embedding, n, c->cap.max_candidates,
                                c->cap.max_detections, c->det, c->P, st));
   ++c->launches;
-  AssocArgs a;
+  AssocArgs a = {};
   a.det = c->det;
   a.trk = c->trk;
   a.trace = to_trace(trace);
@@ -859,7 +946,9 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
   a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
+  a.sclk = (c->profiling & 4) ? c->d_stats + 32 : nullptr;
   a.cluster = 1;
+  set_stream_order(c, a, stream, 1);
   a.out.count = out->count;
   a.out.track_id = reinterpret_cast<long long*>(out->track_id);
   a.out.box = out->box;
@@ -1053,6 +1142,13 @@ int tf_phase_stats(tf_ctx* c, int64_t* out16) {
   TF_CUDA(c, cudaDeviceSynchronize());
   TF_CUDA(c, cudaMemcpy(out16, c->d_stats, 32 * sizeof(long long), cudaMemcpyDeviceToHost));
   TF_CUDA(c, cudaMemset(c->d_stats, 0, 32 * sizeof(long long)));
+  return TF_OK;
+}
+
+int tf_stream_clocks(tf_ctx* c, int64_t* out, int32_t n_streams) {
+  if (!c || !out || n_streams < 0 || n_streams > c->n_streams_alloc) return TF_ARGUMENT;
+  TF_CUDA(c, cudaDeviceSynchronize());
+  TF_CUDA(c, cudaMemcpy(out, c->d_stats + 32, 4 * sizeof(long long) * n_streams, cudaMemcpyDeviceToHost));
   return TF_OK;
 }
 

@@ -14,6 +14,8 @@
 //  stage kernels        batched nms / lap / kalman / gating / cost / normalize /
 //                       binary16 / smooth / iou for the reference's module-level
 //                       functions.
+#include <algorithm>
+#include <climits>
 #include <cooperative_groups.h>
 #include <map>
 #include <mutex>
@@ -92,6 +94,12 @@ struct FrameArgs {
   int frames;
   int cap_cand, cap_det, words;
   DetBuf det;
+  // overlapped mode (ready == nullptr: one CTA per frame)
+  unsigned* ready;               // [frames] the update's epoch once frame f is decoded
+  unsigned epoch;
+  int* ticket;                   // [2] work counter, exit counter (left at 0)
+  const int* order;              // the association's block -> stream order (nullptr = identity)
+  int first_wave, streams, B;
 };
 
 // Shared-memory plan of frame_heads_kernel (bytes computed by frame_smem_bytes()).
@@ -272,17 +280,11 @@ __device__ int gather_normalize(const T* src, long long stride, int dim, int qua
 #else
 #define TF_FT(i)
 #endif
+// One frame: scan, decode, NMS, gather (the body of frame_heads_kernel).
 template <typename T, int kThreads>
-__global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1) frame_heads_kernel(FrameArgs a, Params P) {
+__device__ __forceinline__ void frame_heads_body(const FrameArgs& a, const Params& P, const int f, cg::cluster_group cl,
+                                                 const int CR, const int crank) {
   extern __shared__ __align__(16) unsigned char smem[];
-  // With few frames a thread-block cluster scans each frame: every CTA takes a
-  // share of the anchor groups and stores its ballots into the leader CTA's
-  // shared memory (DSMEM); the leader then ranks, decodes, suppresses and
-  // gathers alone. One CTA per frame (cluster size 1) otherwise.
-  cg::cluster_group cl = cg::this_cluster();
-  const int CR = static_cast<int>(cl.num_blocks());
-  const int crank = static_cast<int>(cl.block_rank());
-  const int f = blockIdx.x / CR;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
 #ifdef TF_FRAME_TIMERS
   long long ft[10] = {0};
@@ -553,6 +555,74 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1)
     a.det.cand_count[f] = C_all;
     int st = s_misc[0];
     a.det.status[f] = (st == STATUS_CLEAR) ? 0 : (st & 0xff);
+  }
+}
+
+// Frame of the i-th visit in overlapped mode: the association's block order
+// (a.order: longest-first when it is used, else identity) in chunks of
+// first_wave blocks, frame-major inside a chunk, so the streams whose CTAs
+// start first get their frames 0, 1, ... first and each association CTA
+// finds its next frame decoded before it needs it.
+__device__ __forceinline__ int visit_frame(const FrameArgs& a, int i) {
+  const int W = a.first_wave, B = a.B;
+  const int chunk = i / (W * B), within = i - chunk * W * B;
+  const int nc = min(W, a.streams - chunk * W);
+  const int b = within / nc;
+  const int p = chunk * W + (within - b * nc);
+  const int ls = a.order ? a.order[p] : p;
+  return ls * B + b;
+}
+
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// With few frames a thread-block cluster scans each frame: every CTA takes a
+// share of the anchor groups and stores its ballots into the leader CTA's
+// shared memory (DSMEM); the leader then ranks, decodes, suppresses and
+// gathers alone. One CTA per frame (cluster size 1) otherwise.
+//
+// Overlapped mode (a.ready != nullptr; many frames, no cluster): a persistent
+// grid takes frames from a work counter in visit_frame order and publishes
+// each finished frame with a release store of the update's epoch into
+// a.ready[f]. The association grid (next on the stream, programmatic
+// dependent launch) starts at once and waits per frame on these flags instead
+// of on this grid's completion, so decode and association overlap within one
+// update. No deadlock: the association is launched only once every CTA of
+// this grid is resident (all of them trigger at entry), and this grid never
+// waits on it.
+template <typename T, int kThreads>
+__global__ void __launch_bounds__(kThreads, kThreads == 256 ? TF_FRAME_MINB : 1) frame_heads_kernel(FrameArgs a, Params P) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CR = static_cast<int>(cl.num_blocks());
+  const int crank = static_cast<int>(cl.block_rank());
+  if (a.ready == nullptr) {
+    frame_heads_body<T, kThreads>(a, P, blockIdx.x / CR, cl, CR, crank);
+    return;
+  }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  __shared__ int s_visit;
+  for (;;) {
+    if (threadIdx.x == 0) s_visit = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int i = s_visit;
+    if (i >= a.frames) break;
+    const int f = visit_frame(a, i);
+    frame_heads_body<T, kThreads>(a, P, f, cl, 1, 0);
+    __syncthreads();                          // every thread's outputs of frame f are written
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release_gpu(a.ready + f, a.epoch);
+    }
+  }
+  if (threadIdx.x == 0 && atomicAdd(a.ticket + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    a.ticket[0] = 0;                          // the last CTA out resets the counters
+    a.ticket[1] = 0;
   }
 }
 
@@ -1186,15 +1256,67 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // streams than twice the SM count (the host halves the shared-memory plan).
 // kExt: the JDE extensions (lambda-fused cost, IoU second stage) are compiled
 // only into their own instantiations, so the reference path keeps its code.
+// Longest-processing-time-first order of n single-CTA streams for the next
+// launch over the same streams, from this launch's per-stream work (cycles of
+// the frame loop): a counting sort into 1024 buckets, heaviest bucket first.
+// Order inside a bucket is arbitrary (it only steers the block scheduler; the
+// results do not depend on it). Run by the last CTA to finish; scratch: 2048
+// ints of shared memory.
+__device__ void lpt_order(const long long* work, int* order, int n, int* scratch) {
+  constexpr int kBuckets = 1024;
+  int* hist = scratch;
+  int* off = scratch + kBuckets;
+  __shared__ long long s_lo, s_hi;
+  const int tid = threadIdx.x;
+  if (tid == 0) { s_lo = LLONG_MAX; s_hi = LLONG_MIN; }
+  for (int i = tid; i < kBuckets; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const long long w = __ldcg(work + i);
+    lo = min(lo, w);
+    hi = max(hi, w);
+  }
+  atomicMin(reinterpret_cast<long long*>(&s_lo), lo);
+  atomicMax(reinterpret_cast<long long*>(&s_hi), hi);
+  __syncthreads();
+  const double span = static_cast<double>(s_hi - s_lo) + 1.0;
+  auto bucket = [&](int i) {
+    const int b = static_cast<int>(static_cast<double>(s_hi - __ldcg(work + i)) * (kBuckets - 1) / span);
+    return min(max(b, 0), kBuckets - 1);
+  };
+  for (int i = tid; i < n; i += blockDim.x) atomicAdd(&hist[bucket(i)], 1);
+  __syncthreads();
+  if (tid < 32) {                             // exclusive scan of the histogram by one warp
+    int run = 0;
+    for (int c = 0; c < kBuckets; c += 32) {
+      const int v = hist[c + tid];
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, o);
+        if (tid >= o) x += y;
+      }
+      off[c + tid] = run + x - v;
+      run += __shfl_sync(FULL, x, 31);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) order[atomicAdd(&off[bucket(i)], 1)] = i;
+}
+
 template <int kThreads, bool kExt>
 __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(AssocArgs a, Params P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const long long t_k0 = clock64();           // launch prologue / epilogue timers (slots 28, 29)
+  auto gtimer = [] { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; };
   const int C = a.cluster;                   // CTAs per stream (thread-block cluster)
-  const int ls = blockIdx.x / C;             // local stream in this update
-  const int s = a.stream_begin + ls;         // global stream id
+  int ls = blockIdx.x / C;                   // local stream in this update (a.order_in: see below)
+  int s = a.stream_begin + ls;               // global stream id
   const int rank = C > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
   const int tid = threadIdx.x, lane = lane_id(), wid = warp_id(), nw = n_warps();
+  long long t_gt0 = 0;
+  if (a.sclk && tid == 0 && rank == 0) t_gt0 = gtimer();
   const int Tm = a.cap_tracks, Km = a.cap_det, D = P.dim;
   const int KW = (Km + 31) / 32;
   const AssocPlan pl = assoc_plan(Tm, Km, a.cap_entries);
@@ -1347,7 +1469,21 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   // works; it waits here for this grid's completion (and its memory) before
   // touching the track tables and embedding pool that this launch writes.
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // Overlapped mode (a.ready): the preceding grid is the decode of this very
+  // update; frames are awaited one by one on its ready flags (below) instead
+  // of on its completion. The track tables were written by the association
+  // before that decode grid, which had completed when the decode grid began.
+  if (a.ready == nullptr) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // Longest-first stream order (single-CTA streams over more than one wave):
+  // the previous launch over these streams ranked them by its measured work
+  // (lpt_order below), so the heaviest streams take the first wave and the
+  // light ones fill the slots that free up. Read only after the wait above:
+  // the previous launch wrote it.
+  if (a.order_in) {
+    ls = a.order_in[blockIdx.x];
+    s = a.stream_begin + ls;
+  }
+  if (a.sclk && tid == 0 && rank == 0) a.sclk[4 * s] = t_gt0;
 
   if (rank != 0) {
     // ---- follower CTA: joins the cost and EMA phases of every frame -------
@@ -1439,12 +1575,36 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   // measurement copy leave the frame's critical path
   __shared__ long long s_fidx[kFrameTable];
   __shared__ int s_fst[kFrameTable], s_fcnt[kFrameTable];
+  const bool await_frames = a.ready != nullptr;   // overlapped mode: frames arrive while this CTA runs
   for (int i = tid; i < a.B && i < kFrameTable; i += blockDim.x) {
     const int fi = ls * a.B + i;
     s_fidx[i] = fi < a.n_fidx_inline ? a.fidx_inline[fi] : a.frame_index[fi];
-    s_fst[i] = a.det.status[fi];
-    s_fcnt[i] = min(a.det.count[fi], Km);
+    if (!await_frames) {
+      s_fst[i] = a.det.status[fi];
+      s_fcnt[i] = min(a.det.count[fi], Km);
+    }
   }
+  // overlapped mode: thread 0 waits for frame b's ready flag (acquire) and
+  // stages its scalars; polls frame b + 1 (its prefetch is issued only if it
+  // is already decoded). The caller's barrier publishes both to the CTA.
+  __shared__ int s_next_ready;
+  auto await_frame = [&](int b) {
+    const int fi = ls * a.B + b;
+    while (ld_acquire_gpu(a.ready + fi) != a.epoch) __nanosleep(256);
+    if (b < kFrameTable) {
+      s_fst[b] = a.det.status[fi];
+      s_fcnt[b] = min(a.det.count[fi], Km);
+    }
+    int nr = 0;
+    if (b + 1 < a.B && ld_acquire_gpu(a.ready + fi + 1) == a.epoch) {
+      nr = 1;
+      if (b + 1 < kFrameTable) {
+        s_fst[b + 1] = a.det.status[fi + 1];
+        s_fcnt[b + 1] = min(a.det.count[fi + 1], Km);
+      }
+    }
+    s_next_ready = nr;
+  };
   auto frame_count = [&](int b) { return b < kFrameTable ? s_fcnt[b] : min(a.det.count[ls * a.B + b], Km); };
   auto prefetch_dets = [&](int b, double* dm, double* dob) {
     // cp.async (LDGSTS): 2 x 16 B of measurement + 8 B objectness per detection
@@ -1459,10 +1619,13 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   __syncthreads();
-  if (a.B > 0) prefetch_dets(0, d_meas0, d_obj0);
+  if (a.B > 0 && !await_frames) prefetch_dets(0, d_meas0, d_obj0);
+  bool have_dets = !await_frames;   // this frame's detections were prefetched
 
   long long t_top = 0;
   if (a.stats && tid == 0) s_ph[28] += clock64() - t_k0;
+  if (a.sclk && tid == 0) a.sclk[4 * s + 1] = gtimer();
+  const long long t_work0 = clock64();
   long long t_epi = 0;
   for (int b = 0; b < a.B; ++b) {
     if (a.stats && tid == 0) {                     // whole-frame cycles (slot 31)
@@ -1471,6 +1634,11 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
       t_top = now_;
     }
     if (s_status != 0) break;                      // stream failed earlier: stop
+    if (await_frames) {
+      if (tid == 0) await_frame(b);
+      __syncthreads();
+      if (!have_dets) prefetch_dets(b, (b & 1) ? d_meas1 : d_meas0, (b & 1) ? d_obj1 : d_obj0);
+    }
     const int f = ls * a.B + b;
     const long long fK = static_cast<long long>(f) * Km;
     const long long frame = b < kFrameTable ? s_fidx[b] : f < a.n_fidx_inline ? a.fidx_inline[f] : a.frame_index[f];
@@ -1490,7 +1658,8 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     d_meas = (b & 1) ? d_meas1 : d_meas0;
     d_obj = (b & 1) ? d_obj1 : d_obj0;
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    if (b + 1 < a.B) prefetch_dets(b + 1, (b & 1) ? d_meas0 : d_meas1, (b & 1) ? d_obj0 : d_obj1);
+    have_dets = b + 1 < a.B && (!await_frames || s_next_ready);
+    if (have_dets) prefetch_dets(b + 1, (b & 1) ? d_meas0 : d_meas1, (b & 1) ? d_obj0 : d_obj1);
     for (int k = tid; k < K; k += blockDim.x) d_row[k] = -1;
     // ---- Kalman predict for every live track (tf/tracker.py:98-99) --------
     const bool gating = (T > 0 && K > 0);
@@ -2428,6 +2597,8 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     }
   }
   if (a.stats && tid == 0) t_epi = clock64();
+  if (a.sclk && tid == 0) a.sclk[4 * s + 2] = gtimer();
+  const long long t_work = clock64() - t_work0;
   asm volatile("cp.async.wait_all;\n" ::: "memory");   // no prefetch outlives an early exit
   __syncthreads();
   // ---- write the stream's state back (the followers' last EMA runs meanwhile) --
@@ -2458,10 +2629,25 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   if (a.stats && tid < 32) atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[tid]),
                                       static_cast<unsigned long long>(s_ph[tid]));
   if (tid == 0) {
+    if (a.sclk) a.sclk[4 * s + 3] = gtimer();
     tb.n_tracks[s] = T;
     tb.next_id[s] = s_next;
     tb.n_free[s] = s_nfree;
     if (s_status) tb.status[s] = s_status;    // sticky until tf_finish reads it
+  }
+  if (a.order_out) {                          // single-CTA streams only (C == 1)
+    __shared__ int s_last;
+    if (tid == 0) {
+      a.work[ls] = t_work;
+      __threadfence();
+      s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {                             // every other CTA has finished: rank the streams
+      __threadfence();
+      lpt_order(a.work, a.order_out, static_cast<int>(gridDim.x), reinterpret_cast<int*>(smem));
+      if (tid == 0) *a.ticket = 0u;
+    }
   }
 }
 
@@ -3014,7 +3200,7 @@ size_t assoc_smem_bytes(int cap_tracks, int cap_det, int cap_entries) {
 }
 
 cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_t st) {
-  FrameArgs a;
+  FrameArgs a = {};
   for (int i = 0; i < 3; ++i) {
     const tf_head_scale& s = h.heads->scale[i];
     a.sc[i].head = h.head_ptr[i];
@@ -3045,6 +3231,13 @@ cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_
   a.cap_det = h.cap_det;
   a.words = (h.cap_cand + 63) / 64;
   a.det = h.det;
+  a.ready = h.ready;
+  a.epoch = h.epoch;
+  a.ticket = h.ticket;
+  a.order = h.order;
+  a.first_wave = h.first_wave;
+  a.streams = h.streams;
+  a.B = h.B;
   int total = 0;
   for (int i = 0; i < 3; ++i) total += 4 * h.heads->scale[i].height * h.heads->scale[i].width;
   const size_t smem = frame_smem_bytes(total, h.cap_cand);
@@ -3053,10 +3246,29 @@ cudaError_t launch_frame_heads(const HeadLaunch& h, const Params& P, cudaStream_
   int cr = 1;                                      // CTAs per frame (cluster) when frames are few
   if (!many)
     while (cr < 8 && h.frames * cr * 2 <= sms) cr *= 2;
+  if (h.ready) cr = 1;                             // overlapped mode: persistent, one CTA per SM slot
   auto go = [&](auto kern, int threads) {
     set_smem(reinterpret_cast<const void*>(kern), smem);
+    // overlapped mode: an association CTA (~110 KB of shared memory) must fit
+    // next to the decode CTAs on an SM, and an SM only hosts CTAs of kernels
+    // whose shared-memory carveout it is configured with, so the decode asks
+    // for the maximum carveout too (otherwise the association waits for SMs
+    // to drain, i.e. for the end of the decode)
+    if (h.ready) {
+      static std::mutex mu;
+      static std::map<std::pair<const void*, int>, bool> done;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::lock_guard<std::mutex> lock(mu);
+      auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+      if (!done[key]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        done[key] = true;
+      }
+    }
     if (cr == 1) {
-      kern<<<h.frames, threads, smem, st>>>(a, P);
+      const int grid = h.ready ? std::min(h.frames, h.persist_ctas) : h.frames;
+      kern<<<grid, threads, smem, st>>>(a, P);
       return;
     }
     cudaLaunchConfig_t cfg = {};

@@ -72,6 +72,13 @@ struct AssocArgs {
   double* pool_val;
   int16_t* pool_aux;             // [streams][2 * cap_tracks * cap_det] overflow edge lists
   long long* stats;              // [32] phase cycles / counters (nullptr = off)
+  const int* order_in;           // [n_streams] block -> local stream (longest first), nullptr = identity
+  int* order_out;                // written by the last CTA for the next launch over these streams (C == 1)
+  long long* work;               // [n_streams] per-stream frame-loop cycles of this launch (order_out)
+  unsigned* ticket;              // CTA completion counter (order_out), left at 0
+  const unsigned* ready;         // overlapped mode: [F] frame f decoded when ready[f] == epoch (nullptr: off)
+  unsigned epoch;
+  long long* sclk;               // [streams][4] leader globaltimer: entry, prologue done, frames done, exit (nullptr = off)
   int cluster;                   // CTAs per stream (1 = no cluster)
   int threads;                   // kAssocThreads, or kAssocThreadsSmall (no cluster)
   int zero_smem;                 // diagnostics (TF_ZERO_SMEM): clear the dynamic shared memory at launch
@@ -85,6 +92,12 @@ struct HeadLaunch {
   long long delta_stride_n[3], delta_stride_c[3];
   int frames, cap_cand, cap_det;
   DetBuf det;
+  // overlapped decode + association (frame_heads_kernel overlapped mode); ready == nullptr: off
+  unsigned* ready;
+  unsigned epoch;
+  int* ticket;
+  const int* order;
+  int first_wave, streams, B, persist_ctas;
 };
 
 size_t frame_smem_bytes(int total_anchors, int cap_cand);

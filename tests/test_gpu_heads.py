@@ -216,6 +216,19 @@ def test_narrow_association_ctas_match_oracle(monkeypatch):
     assert cmp.frames == 6 * 24
 
 
+def test_overlapped_decode_and_association_match_oracle(monkeypatch):
+    """Opt-in overlapped mode (TF_OVERLAP): a persistent decode grid publishes
+    frames through per-frame ready flags and the association, launched as its
+    programmatic dependent, waits per frame instead of on the grid. 40 streams
+    x 8 frames (>= 2 x SMs frames) with 128-thread association CTAs, 3 steps,
+    four streams checked against the oracle."""
+    monkeypatch.setenv("TF_ASSOC_NARROW", "1")
+    monkeypatch.setenv("TF_OVERLAP", "1")
+    cmp = _run_parity("cfg4", steps=3, B=8, streams=40, check_streams=[0, 13, 27, 39], max_candidates=192,
+                      max_detections=96, max_tracks=160, expect_threads=128)
+    assert cmp.frames == 4 * 24
+
+
 @pytest.mark.parametrize("cluster,narrow", [("16", False), ("1", False), ("1", True)])
 def test_pooled_entries_path_matches_oracle(monkeypatch, cluster, narrow):
     """Frames whose gated entries exceed the on-chip capacity keep them in the
