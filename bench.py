@@ -540,7 +540,7 @@ def run_ours(args):
     barrier()
     fr_ms, as_ms, nup = C.c_double(), C.c_double(), C.c_int64()
     lib.tf_kernel_times(eng.ctx, C.byref(fr_ms), C.byref(as_ms), C.byref(nup))
-    phase = np.zeros(32, np.int64)
+    phase = np.zeros(40, np.int64)
     lib.tf_phase_stats(eng.ctx, phase.ctypes.data)
     lib.tf_set_profiling(eng.ctx, 0)
     same_state = None

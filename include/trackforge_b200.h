@@ -261,8 +261,11 @@ int tf_timeline(tf_ctx* ctx, double* out, int32_t max_updates, int32_t* n_update
  * compaction, births; counters [8] tie fallbacks [9] finite entries
  * [10] multi-edge components [11] frames [12] sum T [13] sum K; LAP sub-phases
  * [16] components + tie check [17] peeling [18] residual components
- * [19] warp solves [20] full restatement (ties). out has 32 entries. */
-int tf_phase_stats(tf_ctx* ctx, int64_t* out32);
+ * [19] warp solves [20] full restatement (ties); why the full restatement
+ * ran: [32] a component's uniqueness undecided (> 32 active rows) [33] an
+ * alternative optimum [34] a star's runner-up within eps [35] entries beyond
+ * the int16 edge lists. out has 40 entries. */
+int tf_phase_stats(tf_ctx* ctx, int64_t* out40);
 /* Per-stream association clocks of the last update run with profiling bit 2
  * (tf_set_profiling(ctx, 4 | ...); diagnostics, synchronising): out[4s..4s+3]
  * = the leader CTA's %globaltimer (ns) at entry, after the prologue (state

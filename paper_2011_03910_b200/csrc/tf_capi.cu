@@ -107,7 +107,7 @@ struct tf_ctx {
   size_t events_used;
   double last_h2d_ms;              // host->device copy time of the last tf_kernel_times window
   long long prof_bytes_frame, prof_frames;
-  long long* d_stats;            // [32] phase stats, then [streams][4] leader clocks (profiling bit 2)
+  long long* d_stats;            // [kPhaseSlots] phase stats, then [streams][4] leader clocks (profiling bit 2)
   int n_streams_alloc = 0;
   int sms = 0;                    // SM count of the device
   // longest-first order of single-CTA streams over more than one wave (associate_kernel)
@@ -468,7 +468,7 @@ int tf_create(const tf_config* config, const tf_capacity* capacity, int32_t devi
   A(&c->pool_row, S * Tm * Km);
   A(&c->pool_val, S * Tm * Km);
   A(&c->pool_aux, 2 * S * Tm * Km);
-  A(&c->d_stats, 32 + 4 * S);
+  A(&c->d_stats, kPhaseSlots + 4 * S);
   A(&c->d_order, S);
   A(&c->d_work, S);
   A(&c->d_ticket, 1);
@@ -758,7 +758,7 @@ int tf_update_heads(tf_ctx* c, const tf_heads* heads, int32_t stream_begin, int3
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
   a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
-  a.sclk = (c->profiling & 4) ? c->d_stats + 32 : nullptr;
+  a.sclk = (c->profiling & 4) ? c->d_stats + kPhaseSlots : nullptr;
   {
     const int key = n_streams * 64 + c->env_cluster;
     if (key != c->cluster_key) {
@@ -876,7 +876,7 @@ int tf_update_detections(tf_ctx* c, int32_t stream_begin, int32_t n_streams, int
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
   a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
-  a.sclk = (c->profiling & 4) ? c->d_stats + 32 : nullptr;
+  a.sclk = (c->profiling & 4) ? c->d_stats + kPhaseSlots : nullptr;
   {
     const int key = n_streams * 64 + c->env_cluster;
     if (key != c->cluster_key) {
@@ -946,7 +946,7 @@ int tf_step_detections(tf_ctx* c, int32_t stream, int64_t frame_index, int32_t n
   a.pool_val = c->pool_val;
   a.pool_aux = c->pool_aux;
   a.stats = (c->profiling & 2) ? c->d_stats : nullptr;
-  a.sclk = (c->profiling & 4) ? c->d_stats + 32 : nullptr;
+  a.sclk = (c->profiling & 4) ? c->d_stats + kPhaseSlots : nullptr;
   a.cluster = 1;
   set_stream_order(c, a, stream, 1);
   a.out.count = out->count;
@@ -1133,22 +1133,22 @@ int tf_set_profiling(tf_ctx* c, int32_t enabled) {
   c->prof_counter = 0;
   c->prof_on = true;
   c->events_used = 0;
-  TF_CUDA(c, cudaMemset(c->d_stats, 0, 32 * sizeof(long long)));
+  TF_CUDA(c, cudaMemset(c->d_stats, 0, kPhaseSlots * sizeof(long long)));
   return TF_OK;
 }
 
 int tf_phase_stats(tf_ctx* c, int64_t* out16) {
   if (!c || !out16) return TF_ARGUMENT;
   TF_CUDA(c, cudaDeviceSynchronize());
-  TF_CUDA(c, cudaMemcpy(out16, c->d_stats, 32 * sizeof(long long), cudaMemcpyDeviceToHost));
-  TF_CUDA(c, cudaMemset(c->d_stats, 0, 32 * sizeof(long long)));
+  TF_CUDA(c, cudaMemcpy(out16, c->d_stats, kPhaseSlots * sizeof(long long), cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemset(c->d_stats, 0, kPhaseSlots * sizeof(long long)));
   return TF_OK;
 }
 
 int tf_stream_clocks(tf_ctx* c, int64_t* out, int32_t n_streams) {
   if (!c || !out || n_streams < 0 || n_streams > c->n_streams_alloc) return TF_ARGUMENT;
   TF_CUDA(c, cudaDeviceSynchronize());
-  TF_CUDA(c, cudaMemcpy(out, c->d_stats + 32, 4 * sizeof(long long) * n_streams, cudaMemcpyDeviceToHost));
+  TF_CUDA(c, cudaMemcpy(out, c->d_stats + kPhaseSlots, 4 * sizeof(long long) * n_streams, cudaMemcpyDeviceToHost));
   return TF_OK;
 }
 

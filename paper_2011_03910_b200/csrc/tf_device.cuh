@@ -837,8 +837,10 @@ __device__ __forceinline__ bool lap_no_active_rows(int nr, int nc, const Transpo
 }
 
 template <class Rows>
-__device__ inline bool lap_unique(int nr, int nc, const Rows R, double sentinel, double eps, LapScratch s) {
-  if (lap_no_active_rows(nr, nc, R, sentinel, eps, s)) return true;
+// Returns 1: unique; 0: an alternative exists; -1: undecided (more than 32
+// active rows) -- the caller treats both 0 and -1 as "solve the whole matrix".
+__device__ inline int lap_unique(int nr, int nc, const Rows R, double sentinel, double eps, LapScratch s) {
+  if (lap_no_active_rows(nr, nc, R, sentinel, eps, s)) return 1;
   const int lane = lane_id();
   for (int j = lane; j < nc; j += 32) s.row4col[j] = -1;
   __syncwarp();
@@ -869,8 +871,8 @@ __device__ inline bool lap_unique(int nr, int nc, const Rows R, double sentinel,
     m += __popc(bm);
   }
   __syncwarp();
-  if (m == 0) return true;
-  if (m > 32) return false;
+  if (m == 0) return 1;
+  if (m > 32) return -1;
   // the graph on the active rows: lane a = active row row_of[a]
   unsigned A = 0u, FA = 0u;
   bool to_free = false, ftofree = false, fm = false, freeable = false;
@@ -918,7 +920,7 @@ __device__ inline bool lap_unique(int nr, int nc, const Rows R, double sentinel,
       if (from_start && ((fr_reach >> k) & 1u)) alt = true;
     }
   }
-  return !__any_sync(FULL, alt);
+  return __any_sync(FULL, alt) ? 0 : 1;
 }
 
 }  // namespace tfd

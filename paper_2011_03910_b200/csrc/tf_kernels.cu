@@ -1402,7 +1402,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   int* f_stk = reinterpret_cast<int*>(smem + pl.off_fstk);
 
   // optional phase timing (tf_set_profiling): cycles per phase + counters
-  __shared__ long long s_ph[32];
+  __shared__ long long s_ph[kPhaseSlots];
   long long t_mark = 0, t_sub = 0;
 #define TF_SUB(i)                                     \
   if (a.stats && tid == 0) {                          \
@@ -1434,7 +1434,7 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
     t_sub = now_;                                     \
   }
   long long t_frame0 = 0;
-  if (tid < 32) s_ph[tid] = 0;
+  for (int x = tid; x < kPhaseSlots; x += blockDim.x) s_ph[x] = 0;
   __shared__ long long s_next;
   __shared__ double s_amp;
   __shared__ double s_ampw[128];    // per-worker cost maxima (cluster warps <= 128)
@@ -2029,7 +2029,10 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
         c_elist = c_epos;
         c_epos = tmp;
       }
-      if (tid == 0) { s_tie = huge; s_alt = 0; s_nmulti = -1; }
+      if (tid == 0) {
+        s_tie = huge; s_alt = 0; s_nmulti = -1;
+        if (a.stats && huge) s_ph[35] += 1;
+      }
       if (!huge && E_live <= 32) {
         // Small residual (the common case): one warp labels the components,
         // checks them for equal costs and lays out the per-component problems;
@@ -2213,7 +2216,10 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) second = fmin(second, __shfl_xor_sync(FULL, second, o));
             if (lane == 0 && be >= 0) rcol[erow[be]] = ecol[be];
-            if (lane == 0 && !(second - best > tie_eps)) s_alt = 1;
+            if (lane == 0 && !(second - best > tie_eps)) {
+              s_alt = 1;
+              if (a.stats) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ph[34]), 1ull);
+            }
             continue;
           }
           int nr_l = 0, nc_l = 0;
@@ -2279,9 +2285,13 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
             if (a.stats && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ph[14]), 1ull);
 #endif
 #ifndef TF_EXPERIMENT_NO_LAPU
-            if (!lap_unique(nc_l, n_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, tie_eps, Ls) &&
-                lane == 0)
-              s_alt = 1;
+            {
+              const int uq = lap_unique(nc_l, n_l, TransposedRows{lrp, led, erow, eval, c_rmap}, sentinel, tie_eps, Ls);
+              if (uq <= 0 && lane == 0) {
+                s_alt = 1;
+                if (a.stats) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ph[uq < 0 ? 32 : 33]), 1ull);
+              }
+            }
 #endif
             for (int j = lane; j < nc_l; j += 32) {
               const int lc = Ls.col4row[j];
@@ -2298,9 +2308,14 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
             if (a.stats && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ph[10]), 1ull);
 #endif
 #ifndef TF_EXPERIMENT_NO_LAPU
-            if (!lap_unique(nr_l, n_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel, tie_eps,
-                            Ls) && lane == 0)
-              s_alt = 1;
+            {
+              const int uq = lap_unique(nr_l, n_l, ComponentRows{rowptr, ecol, eval, c_rows + off, c_map}, sentinel,
+                                        tie_eps, Ls);
+              if (uq <= 0 && lane == 0) {
+                s_alt = 1;
+                if (a.stats) atomicAdd(reinterpret_cast<unsigned long long*>(&s_ph[uq < 0 ? 32 : 33]), 1ull);
+              }
+            }
 #endif
             for (int r = lane; r < nr_l; r += 32) {
               const int j = Ls.col4row[r];
@@ -2626,8 +2641,8 @@ __global__ void __launch_bounds__(kThreads, 256 / kThreads) associate_kernel(Ass
   }
   if (a.stats && tid == 0) s_ph[29] += clock64() - t_epi;
   __syncthreads();
-  if (a.stats && tid < 32) atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[tid]),
-                                      static_cast<unsigned long long>(s_ph[tid]));
+  if (a.stats && tid < kPhaseSlots) atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[tid]),
+                                               static_cast<unsigned long long>(s_ph[tid]));
   if (tid == 0) {
     if (a.sclk) a.sclk[4 * s + 3] = gtimer();
     tb.n_tracks[s] = T;

@@ -57,6 +57,8 @@ struct TraceBuf {
   int* det_matched;
 };
 
+constexpr int kPhaseSlots = 40;   // associate_kernel phase timers / counters (tf_phase_stats)
+
 struct AssocArgs {
   DetBuf det;
   TrackBuf trk;
@@ -71,7 +73,7 @@ struct AssocArgs {
   int16_t* pool_row;
   double* pool_val;
   int16_t* pool_aux;             // [streams][2 * cap_tracks * cap_det] overflow edge lists
-  long long* stats;              // [32] phase cycles / counters (nullptr = off)
+  long long* stats;              // [kPhaseSlots] phase cycles / counters (nullptr = off)
   const int* order_in;           // [n_streams] block -> local stream (longest first), nullptr = identity
   int* order_out;                // written by the last CTA for the next launch over these streams (C == 1)
   long long* work;               // [n_streams] per-stream frame-loop cycles of this launch (order_out)

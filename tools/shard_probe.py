@@ -46,7 +46,7 @@ lib.tf_launch_info(bt.engine.ctx, C.byref(th), C.byref(cl))
 lib.tf_set_profiling(bt.engine.ctx, 2)
 b = gen.next_batch(8)
 bt.update(b)
-ph = np.zeros(32, np.int64)
+ph = np.zeros(40, np.int64)
 lib.tf_phase_stats(bt.engine.ctx, ph.ctypes.data)
 names = ["load_predict", "gate", "csr", "cost", "lap", "match", "update_ema", "records_births"]
 print(json.dumps({"streams": S, "threads": th.value, "cluster": cl.value, "ms_per_step": ms / K,
