@@ -366,18 +366,34 @@ def timed_updates(bt, batches, stream, lib):
     return e0.elapsed_time(e1)
 
 
-def streamed_updates(bt, gen_batch, K, F, stream, trace_counts):
-    """K updates of batches generated between steps, each timed alone (events)."""
+def streamed_updates(bt, gen_batch, K, F, stream, trace_counts, host_us=None):
+    """K updates of batches generated between steps, each timed alone (events).
+
+    The stream is held (tf_stream_hold) until update() has queued all of its
+    work, so the events time the device work of the update, not the host's
+    submission of it (~0.1-0.2 ms of Python + C per update at 64-512 streams,
+    which a producer that queues ahead hides); the host time is returned in
+    ``host_us``."""
     import torch
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lib = bt.engine.lib
+    flag = torch.zeros(1, dtype=torch.int32).pin_memory()
     ms = 0.0
     for _ in range(K):
         nb = gen_batch()
         torch.cuda.synchronize()
+        flag.zero_()
+        bt.engine.check(lib.tf_stream_hold(flag.data_ptr(), stream.cuda_stream), "hold")
         e0.record(stream)
-        r = bt.update(nb, trace=True, sync=False)
-        e1.record(stream)
+        try:
+            t0 = time.perf_counter()
+            r = bt.update(nb, trace=True, sync=False)
+            if host_us is not None:
+                host_us.append(1e6 * (time.perf_counter() - t0))
+            e1.record(stream)
+        finally:
+            flag.fill_(1)                  # release the stream (always)
         e1.synchronize()
         ms += e0.elapsed_time(e1)
         tr = bt.trace(F)
@@ -414,7 +430,8 @@ def cfg4_block(args, world, rank, dev, barrier, shard_world=None):
         del nb
     barrier()
     bt.engine.lib.tf_set_profiling(bt.engine.ctx, 1)
-    ms = streamed_updates(bt, lambda: gen.next_batch(B), args.cfg4_steps, F, stream, counts)
+    host_us = []
+    ms = streamed_updates(bt, lambda: gen.next_batch(B), args.cfg4_steps, F, stream, counts, host_us)
     f_ms, a_ms, n = C.c_double(), C.c_double(), C.c_int64()
     bt.engine.lib.tf_kernel_times(bt.engine.ctx, C.byref(f_ms), C.byref(a_ms), C.byref(n))
     bt.engine.finish()
@@ -435,6 +452,8 @@ def cfg4_block(args, world, rank, dev, barrier, shard_world=None):
     return {"streams": cfg.streams, "streams_per_rank": S, "B": B, "steps": args.cfg4_steps,
             "warmup": args.cfg4_warmup, "frames_per_s": summ["frames_per_s"], "ms_per_step": step_ms,
             "gpus_active": len(per_rank), "scaling": "strong",
+            "timing": "device time of each update with its launches pre-queued (stream held until update() returns)",
+            "host_submit_us_per_update": statistics.mean(host_us) if host_us else None,
             "rank0_kernels_ms_per_step": {"frame_heads_kernel": f_ms.value / max(n.value, 1),
                                           "associate_kernel": a_ms.value / max(n.value, 1)},
             "roofline": {"achieved_GBps": ach, "peak_GBps": peak * len(per_rank),

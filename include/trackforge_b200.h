@@ -271,6 +271,12 @@ int tf_phase_stats(tf_ctx* ctx, int64_t* out40);
  * = the leader CTA's %globaltimer (ns) at entry, after the prologue (state
  * loaded), after the last frame, and at exit. n_streams <= the context's. */
 int tf_stream_clocks(tf_ctx* ctx, int64_t* out, int32_t n_streams);
+/* Benchmark support: hold `cuda_stream` until the host stores a non-zero
+ * value into *flag (flag: host memory allocated mapped / pinned, passed as its
+ * device alias), so that an update queued behind the hold runs with all of its
+ * launches already queued (bench.py times single updates this way: the host's
+ * submission time is reported beside the device time, not inside it). */
+int tf_stream_hold(const volatile int32_t* flag, void* cuda_stream);
 
 /* ---- stage-level entry points (batched; device pointers) ---------------- */
 

@@ -96,6 +96,7 @@ _SIGS = {
                                      C.POINTER(TfRecords), C.POINTER(TfTrace), c_vp]),
     "tf_phase_stats": (c_i32, [c_vp, c_vp]),
     "tf_stream_clocks": (c_i32, [c_vp, c_vp, c_i32]),
+    "tf_stream_hold": (c_i32, [c_vp, c_vp]),
     "tf_nms_sets": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tf_lap_dense": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "tf_kalman": (c_i32, [c_i32, c_i32, C.POINTER(TfConfig), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

