@@ -271,6 +271,67 @@ def test_narrow_and_wide_association_agree(monkeypatch):
             assert np.array_equal(np.nan_to_num(k1[f, :n]), np.nan_to_num(k2[f, :n]))
 
 
+def test_longest_first_order_does_not_change_results(monkeypatch):
+    """More single-CTA streams than resident association slots: from the
+    second update on, blocks take streams in longest-first order (lpt_order).
+    Records, costs and the final track tables are bit-identical to the
+    identity order (TF_NO_LPT)."""
+    import torch
+
+    p, synth = _pkg()
+    S, B = 2 * torch.cuda.get_device_properties(0).multi_processor_count + 24, 2
+    outs = []
+    for no_lpt in (False, True):
+        monkeypatch.delenv("TF_NO_LPT", raising=False)
+        if no_lpt:
+            monkeypatch.setenv("TF_NO_LPT", "1")
+        gen = synth.make("cfg4", device="cuda", streams=S, seed=11)
+        cap = p.Capacity(streams=S, max_frames=S * B, max_candidates=192, max_detections=96, max_tracks=160)
+        bt = p.BatchTracker(S, frames_per_update=B, capacity=cap)
+        assert _launch_info(bt)[0] == 128
+        res = []
+        for _ in range(3):
+            b = gen.next_batch(B)
+            r = bt.update(b, trace=True)
+            tr = bt.trace(S * B)
+            res.append((r.count.cpu().numpy().copy(), r.track_id.cpu().numpy().copy(), r.box.cpu().numpy().copy(),
+                        tr["det_cost"].cpu().numpy().copy()))
+            del b
+        res.append([bt.export(s) for s in (0, S // 2, S - 1)])
+        outs.append(res)
+        del bt, gen
+        torch.cuda.empty_cache()
+    for (c1, i1, b1, k1), (c2, i2, b2, k2) in zip(outs[0][:3], outs[1][:3]):
+        assert np.array_equal(c1, c2)
+        assert np.array_equal(i1, i2) and np.array_equal(b1, b2)
+        assert np.array_equal(np.nan_to_num(k1), np.nan_to_num(k2))
+    for e1, e2 in zip(outs[0][3], outs[1][3]):
+        assert all(np.asarray(e1[k]).tobytes() == np.asarray(e2[k]).tobytes() for k in e1)
+
+
+def test_stream_hold_releases():
+    """tf_stream_hold: work queued behind the hold runs only after the host
+    releases the pinned flag (bench.py's single-update timing)."""
+    import time
+
+    import torch
+    from paper_2011_03910_b200 import _lib
+
+    lib = _lib.load()
+    flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+    x = torch.zeros(1, device="cuda")
+    st = torch.cuda.current_stream()
+    assert lib.tf_stream_hold(flag.data_ptr(), st.cuda_stream) == 0
+    x += 1
+    done = torch.cuda.Event()
+    done.record(st)
+    time.sleep(0.05)
+    assert not done.query()              # still held
+    flag.fill_(1)
+    done.synchronize()
+    assert float(x.item()) == 1.0
+
+
 def _run_ext(cfg_name, config, **kw):
     """_run_parity, also returning the oracle's IoU-stage match count."""
     import oracle.tracker as ot
