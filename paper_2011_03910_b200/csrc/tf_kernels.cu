@@ -1135,10 +1135,85 @@ struct EmaView {
   int K, D;
 };
 
+// One matched detection's EMA from rows already in registers (D = 512):
+// normalize(alpha * old + beta * new) in fp64, fp32 out.
+__device__ __forceinline__ void ema_row512(const EmaView& v, int k, int sl, const float4 (&x)[4], const float4 (&y)[4]) {
+  const int lane = lane_id();
+  double w[16];
+  double ss = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    w[4 * q + 0] = v.alpha * static_cast<double>(x[q].x) + v.beta * static_cast<double>(y[q].x);
+    w[4 * q + 1] = v.alpha * static_cast<double>(x[q].y) + v.beta * static_cast<double>(y[q].y);
+    w[4 * q + 2] = v.alpha * static_cast<double>(x[q].z) + v.beta * static_cast<double>(y[q].z);
+    w[4 * q + 3] = v.alpha * static_cast<double>(x[q].w) + v.beta * static_cast<double>(y[q].w);
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) ss = fma(w[q], w[q], ss);
+  ss = warp_sum(ss);
+  const double nrm = sqrt(ss);
+  if (!(nrm >= 1e-12) || !isfinite(nrm)) {
+    if (lane == 0) flag_error(v.err, k + 1, TF_DEGENERATE_EMBEDDING);
+    return;
+  }
+  float4* o4 = reinterpret_cast<float4*>(v.pool + static_cast<long long>(sl) * 512);
+  const double rn = __drcp_rn(nrm);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float4 r;
+    r.x = static_cast<float>(div_by(w[4 * q + 0], nrm, rn));
+    r.y = static_cast<float>(div_by(w[4 * q + 1], nrm, rn));
+    r.z = static_cast<float>(div_by(w[4 * q + 2], nrm, rn));
+    r.w = static_cast<float>(div_by(w[4 * q + 3], nrm, rn));
+    o4[lane + 32 * q] = r;
+  }
+}
+
 // EMA appearance update (tf/tracker.py:67-71, 117-119): one warp per matched
 // detection, normalize(alpha * old + (1 - alpha) * new) in fp64, fp32 out.
+// D = 512: a warp claims two detections at a time and has both pairs of rows
+// in flight before it computes either (one round trip per two items).
 __device__ void ema_work(const EmaView v) {
   const int lane = lane_id();
+#ifndef TF_EMA_SINGLE
+  if (v.D == 512) {
+    // two detections per claim: the second's rows are prefetched into L1
+    // while the first is computed, so its loads do not wait a round trip
+    for (;;) {
+      int k0 = 0;
+      if (lane == 0) k0 = atomicAdd(v.work, 2);
+      k0 = __shfl_sync(FULL, k0, 0);
+      if (k0 >= v.K) return;
+      int s0 = -1, s1 = -1;
+      if (lane == 0) {
+        s0 = v.slot[k0];
+        s1 = k0 + 1 < v.K ? v.slot[k0 + 1] : -1;
+      }
+      s0 = __shfl_sync(FULL, s0, 0);
+      s1 = __shfl_sync(FULL, s1, 0);
+      if (s1 >= 0) {
+        const float* t = v.pool + static_cast<long long>(s1) * 512;
+        const float* d = v.dets + static_cast<long long>(k0 + 1) * 512;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(t + 4 * (lane + 32 * q)));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(d + 4 * (lane + 32 * q)));
+        }
+      }
+#pragma unroll 1
+      for (int i = 0; i < 2; ++i) {
+        const int k = k0 + i, sl = i ? s1 : s0;
+        if (sl < 0) continue;
+        const float4* t4 = reinterpret_cast<const float4*>(v.pool + static_cast<long long>(sl) * 512);
+        const float4* d4 = reinterpret_cast<const float4*>(v.dets + static_cast<long long>(k) * 512);
+        float4 x[4], y[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { x[q] = t4[lane + 32 * q]; y[q] = d4[lane + 32 * q]; }
+        ema_row512(v, k, sl, x, y);
+      }
+    }
+  }
+#endif
   for (;;) {
     int k = 0;
     if (lane == 0) k = atomicAdd(v.work, 1);
