@@ -92,6 +92,33 @@ def test_lap_large_random_vs_restated_solver(p):
         assert col.tolist() == want
 
 
+def test_lap_beyond_register_solver_vs_restated_solver(p):
+    """n > 256: the shared-memory warp solver (config 2's full-matrix tie solves, n ~ 260),
+    sparse gated matrices and integer matrices full of ties, against scipy's order."""
+    from paper_2011_03910_b200.assoc import solve_batch
+    rng = np.random.default_rng(11)
+    mats = []
+    for n in (257, 270, 300, 400):
+        c = rng.uniform(0, 2, (n, n - 40))
+        c[rng.random(c.shape) < 0.95] = np.inf
+        mats.append(c)
+        mats.append(rng.integers(0, 3, (n - 5, n)).astype(float))
+        t = np.round(rng.uniform(0, 2, (n - 120, n)), 1)            # sparse with ties
+        t[rng.random(t.shape) < 0.97] = np.inf
+        mats.append(t)
+    cols = solve_batch(mats)
+    for m, col in zip(mats, cols):
+        nr, nc = m.shape
+        n = max(nr, nc)
+        fin = m[np.isfinite(m)]
+        amp = float(np.max(np.abs(fin))) if fin.size else 1.0
+        pad = np.full((n, n), 2.0 * n * max(amp, 1.0) + 1.0)
+        pad[:nr, :nc] = np.where(np.isfinite(m), m, pad[:nr, :nc])
+        c4r, _ = olap.solve_square(pad)
+        want = [int(c4r[r]) if c4r[r] < nc and math.isfinite(m[r, c4r[r]]) else -1 for r in range(nr)]
+        assert col.tolist() == want, (nr, nc)
+
+
 def test_kalman_sequences_match_reference(p):
     u = load_units()
     kf = p.KalmanFilter()
