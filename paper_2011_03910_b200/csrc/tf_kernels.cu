@@ -818,12 +818,23 @@ __host__ __device__ inline AssocPlan assoc_plan(int T, int K, int E) {
 
 
 // ---- JDE extensions (off on the reference path; SURVEY.md section 8 name map)
+// Both phases are inlined into the extension instantiation (its own register
+// allocation; the reference path never calls them): out of line, the calls
+// made the caller save its live registers around them (436 B of spills, --jde
+// 26.7k frames/s; inlined: 140 B, 28.7k; profiles/r02s_jde_inline_ab.txt).
+// -DTF_JDE_*_ATTR=__noinline__ restores the out-of-line form.
+#ifndef TF_JDE_FUSE_ATTR
+#define TF_JDE_FUSE_ATTR __forceinline__
+#endif
+#ifndef TF_JDE_IOU_ATTR
+#define TF_JDE_IOU_ATTR __forceinline__
+#endif
 
 // lambda-fused cost (JDE fuse_motion): every un-gated entry becomes
 // lambda * cosine + (1 - lambda) * gate distance, the distance recomputed with
 // the gate phase's arithmetic. Called by every thread of the leader; leaves
 // the per-warp maxima of the fused costs in ampw[0 .. n_slots).
-__device__ __noinline__ void fuse_motion_costs(double lambda, double lambda_w, int gate_metric, const int16_t* ecol,
+__device__ TF_JDE_FUSE_ATTR void fuse_motion_costs(double lambda, double lambda_w, int gate_metric, const int16_t* ecol,
                                                const int16_t* erow, double* eval, int E, const double* t_mean,
                                                const double* g_il, const double* d_meas, double* ampw, int n_slots) {
   double m = 0.0;
@@ -864,7 +875,7 @@ struct DenseRows {
 // predicted track state and from the detections' measurements. The same exact
 // solve as the first stage (sentinel padding, scipy order), then pairs above
 // iou_threshold are dissolved. One warp.
-__device__ __noinline__ void iou_second_stage(double thr, int T, int K, int Tm, int Km, int cap_entries,
+__device__ TF_JDE_IOU_ATTR void iou_second_stage(double thr, int T, int K, int Tm, int Km, int cap_entries,
                                               unsigned char* smem, const double* d_meas, double* dense_global,
                                               int* err) {
   const int lane = lane_id();
